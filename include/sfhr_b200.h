@@ -1,0 +1,145 @@
+/*
+ * sfhr_b200 — C-ABI of the B200-native Safhire server hot path.
+ *
+ * Plain pointers and sizes only.  Unless stated otherwise, ciphertext
+ * buffers are DEVICE pointers to little-endian uint64 arrays laid out exactly
+ * like the reference's numpy batches: (rows, 2, N) C-contiguous, values < 2^53
+ * (reference pkg/src/sfhr/crypto.py:404-406, tracepack.py:118-123).  Every
+ * call that launches work takes a cudaStream_t passed as `void* stream`
+ * (NULL = legacy default stream) and is asynchronous on it.
+ *
+ * Return codes map onto the reference's exception types in the Python shim
+ * (paper_2509_01253_b200/_native.py):
+ *   SFHR_EINVAL -> ValueError, SFHR_EKEY -> KeyError, SFHR_EMODEL -> ModelError,
+ *   SFHR_ECUDA/SFHR_ENOMEM -> RuntimeError.  sfhr_last_error() returns the
+ *   message of the calling thread's last failure.
+ *
+ * Thread safety: a context may be used from several host threads; calls are
+ * serialised per context by an internal mutex (the reference runs one thread
+ * per TCP connection, transport.py:136-156).
+ */
+#ifndef SFHR_B200_H
+#define SFHR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SFHR_OK = 0,
+  SFHR_EINVAL = 1,
+  SFHR_EKEY = 2,
+  SFHR_ECUDA = 3,
+  SFHR_EMODEL = 4,
+  SFHR_ENOMEM = 5
+};
+
+typedef struct sfhr_ctx sfhr_ctx;
+typedef struct sfhr_key sfhr_key;
+
+/* Ring row + gadget + levels.  device = -1 creates a planning-only context
+ * (no GPU required; compute entry points then return SFHR_EINVAL).  Replaces the parameter plumbing of
+ * SchemeParams / KeySwitchEngine.__init__ (reference params.py:117-164,
+ * crypto.py:370-382); validates like RingParams/GadgetParams/SchemeParams.
+ * Uploads NTT twiddles to `device`. */
+int sfhr_ctx_create(int t, int alpha, int p_bits, int D, int l, int gamma, int beta,
+                    int device, sfhr_ctx** out);
+int sfhr_ctx_destroy(sfhr_ctx* ctx);
+
+/* info[0..]: M, N, n1, np (CRT primes), pack_factor, beta_eff, shrink,
+ * inv_m_mod_p, cu (as int64), primes[0..np), bound_bits*1000, crt_bits*1000.
+ * Returns the number of entries written (<= n). */
+int sfhr_ctx_info(const sfhr_ctx* ctx, int64_t* info, int n);
+
+/* Debug/verification: copy the device constant block (RingConst, size
+ * sfhr_ringconst_bytes()) and the [np][M+1] Montgomery twiddle table. */
+size_t sfhr_ringconst_bytes(void);
+int sfhr_ctx_debug_tables(const sfhr_ctx* ctx, void* ringconst, size_t rc_bytes, uint32_t* twid,
+                          size_t twid_words);
+
+/* Two-term dual basis (reference dual.py:108-166): host arrays of length N. */
+int sfhr_ctx_dual(const sfhr_ctx* ctx, int32_t* e1, int32_t* e2, int32_t* ratio_len);
+
+/* Register a key-switching key set.  Replaces KeySwitchEngine's spectra cache
+ * (reference crypto.py:384-398) as built by ServerEngine.register_client
+ * (protocol.py:182-194).  idx: host array of nidx automorphism indices;
+ * ksk: DEVICE (nidx, l, 2, N) uint64, keys[idx[s]][i].a / .b. */
+int sfhr_register_ksk(sfhr_ctx* ctx, const uint32_t* idx, int nidx, const uint64_t* ksk,
+                      void* stream, sfhr_key** out);
+int sfhr_key_destroy(sfhr_key* key);
+
+/* KeySwitchEngine.automorphism_batch (reference crypto.py:400-402). */
+int sfhr_automorphism_batch(sfhr_ctx* ctx, uint32_t d, const uint64_t* in, uint64_t* out,
+                            int64_t B, void* stream);
+
+/* KeySwitchEngine.switch_batch (reference crypto.py:404-421): `in` is the
+ * already-automorphed batch.  counter (DEVICE u64, may be NULL) is increased
+ * by the number of switched rows (live rows only when skip_zero). */
+int sfhr_keyswitch_batch(sfhr_ctx* ctx, const sfhr_key* key, uint32_t d, const uint64_t* in,
+                         uint64_t* out, int64_t B, int skip_zero,
+                         unsigned long long* counter, void* stream);
+
+/* tracepack._apply_stage_batch (reference tracepack.py:268-285):
+ * out = in + sum_{rep in reps[1:]} KS_rep(aut_rep(in)).  reps: host array
+ * (reps[0] must be 1).  in and out must not alias. */
+int sfhr_stage_batch(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nreps,
+                     const uint64_t* in, uint64_t* out, int64_t B, int skip_zero,
+                     unsigned long long* counter, void* stream);
+
+/* tracepack.partial_extract for k_chunks bundles + ServerEngine._extract
+ * concatenation (reference tracepack.py:118-154, protocol.py:282-294).
+ * power: DEVICE (k_chunks, npow, 2, N), exponents ascending; exps: host
+ * array; rows: DEVICE (E, 2, N), row j*N + i = coefficient i of chunk j. */
+int sfhr_extract(sfhr_ctx* ctx, const uint64_t* power, const uint32_t* exps, int npow,
+                 int k_chunks, int64_t E, uint64_t* rows, void* stream);
+
+/* One pass of the lowered round map (reference model.py:384-429 semantics;
+ * see paper_2509_01253_b200/model.py LinearPass).  All pointers DEVICE. */
+typedef struct {
+  const uint64_t* in;        /* pass input rows */
+  const int64_t* in_map;     /* optional physical row of each pass-input column */
+  const uint64_t* round_in;  /* round input rows (residual extras) */
+  const int64_t* round_map;  /* optional physical row of each round-input column */
+  uint64_t* out;             /* output rows */
+  const int64_t* out_map;    /* optional physical output row per canonical row */
+  const int32_t* groups;     /* (n_groups, 6) */
+  int64_t n_groups;
+  const int32_t* cols;
+  const int32_t* weights;    /* [ncols][16] blocks */
+  const int32_t* rows;
+  const int32_t* ex_ptr;     /* optional CSR extras */
+  const int32_t* ex_col;
+  const int32_t* ex_w;
+  const int64_t* bias;       /* optional */
+  const uint64_t* unit;      /* (N,) bias unit payload, tracepack.py:157-172 */
+  int64_t lanes;             /* u64 lanes per row; 0 = 2N (ciphertext rows) */
+  int64_t body_off;          /* first lane receiving bias*unit (N for ciphertext rows) */
+} sfhr_linear_desc;
+int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* desc, void* stream);
+
+/* ServerEngine._pack / tracepack.pack_rows + fast_pack (reference
+ * protocol.py:296-321, tracepack.py:288-348) for n_groups zero-padded groups
+ * of pack_factor rows.  rows (DEVICE, n_groups*F rows) is used as scratch and
+ * clobbered; workspace: sfhr_pack_workspace_bytes(); packs: DEVICE
+ * (n_groups, 2, N).  counter (DEVICE u64) += key switches (live rows only
+ * when skip_zero, as ServerEngine._pack does). */
+size_t sfhr_pack_workspace_bytes(const sfhr_ctx* ctx, int64_t n_groups);
+int sfhr_pack(sfhr_ctx* ctx, const sfhr_key* key, uint64_t* rows, int64_t n_groups,
+              uint64_t* packs, void* workspace, size_t workspace_bytes, int skip_zero,
+              unsigned long long* counter, void* stream);
+
+/* confidentiality.derive_permutation (reference confidentiality.py:27-76),
+ * bit-exact: blake2b keyed tree + counter-mode PRF + descending Fisher-Yates.
+ * Host-only; out: host int64[size]. */
+int sfhr_derive_permutation(const uint8_t* master_seed, int seed_len, const uint8_t* session_id,
+                            int sid_len, uint32_t round_no, int64_t size, int64_t* out);
+
+const char* sfhr_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFHR_B200_H */

@@ -1,0 +1,399 @@
+// extern "C" boundary of libsfhr_b200.so (declared in include/sfhr_b200.h).
+// Host orchestration of the pack schedule lives here; all compute is in the
+// kernels of keyswitch.cu / ring_ops.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sfhr_b200.h"
+#include "plan.h"
+#include "sfhr_kernels.h"
+
+namespace sfhr {
+void derive_permutation(const uint8_t* seed, int seed_len, const uint8_t* sid, int sid_len,
+                        uint32_t round_no, int64_t size, int64_t* out);
+}
+
+using namespace sfhr;
+
+struct sfhr_ctx {
+  Plan plan;
+  int device = 0;
+  uint32_t* twid = nullptr;  // [np][M+1]
+  int32_t* cvec = nullptr;   // [N]
+  std::mutex mu;
+};
+
+struct sfhr_key {
+  sfhr_ctx* ctx = nullptr;
+  std::map<uint32_t, int> slot;  // d -> slot
+  uint32_t* spectra = nullptr;   // [nidx][l][2][np][N]
+  size_t slot_words = 0;
+};
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SFHR_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CK(call, where)                          \
+  do {                                           \
+    cudaError_t _e = (call);                     \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int key_slot(const sfhr_key* key, uint32_t d) {
+  const uint32_t M = (uint32_t)key->ctx->plan.rc.M;
+  auto it = key->slot.find(d % M);
+  if (it == key->slot.end()) return -1;
+  return it->second;
+}
+
+int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nreps, int identity,
+              const uint64_t* in, uint64_t* out, int64_t B, int skip_zero,
+              unsigned long long* counter, cudaStream_t st) {
+  const Plan& P = ctx->plan;
+  StageArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.in = in;
+  a.out = out;
+  a.B = B;
+  a.identity = identity;
+  a.skip_zero = skip_zero;
+  a.shrink = P.shrink;
+  a.twid = ctx->twid;
+  a.counter = counter;
+  int ns = 0;
+  for (int r = 0; r < nreps; ++r) {
+    const uint32_t d = reps[r] % (uint32_t)P.rc.M;
+    if (identity && r == 0) {
+      if (d != 1) return fail(SFHR_EINVAL, "stage representatives must start with the identity");
+      continue;
+    }
+    if (ns >= MAXREPS) return fail(SFHR_EINVAL, "too many representatives in one stage");
+    const int s = key_slot(key, d);
+    if (s < 0) return fail(SFHR_EKEY, "key-switch key set has no index " + std::to_string(d));
+    a.spec[ns] = key->spectra + (size_t)s * key->slot_words;
+    a.dinv[ns] = identity ? inv_mod_M(P, d) : 1u;
+    ++ns;
+  }
+  a.nreps = ns;
+  if (ns == 0) {
+    if (in != out) CK(cudaMemcpyAsync(out, in, (size_t)B * 2 * P.rc.N * 8, cudaMemcpyDeviceToDevice, st), "stage copy");
+    return SFHR_OK;
+  }
+  CK(launch_stage(P.rc, a, st), "stage kernel");
+  return SFHR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* sfhr_last_error(void) { return g_err.c_str(); }
+
+int sfhr_ctx_create(int t, int alpha, int p_bits, int D, int l, int gamma, int beta, int device,
+                    sfhr_ctx** out) {
+  if (!out) return fail(SFHR_EINVAL, "null output pointer");
+  sfhr_ctx* ctx = new (std::nothrow) sfhr_ctx();
+  if (!ctx) return fail(SFHR_ENOMEM, "out of host memory");
+  try {
+    ctx->plan = make_plan(t, alpha, p_bits, D, l, gamma, beta);
+  } catch (const std::exception& e) {
+    delete ctx;
+    return fail(SFHR_EINVAL, e.what());
+  }
+  ctx->device = device;
+  if (device < 0) {  // planning-only context (no GPU needed): info/dual/debug tables
+    *out = ctx;
+    return SFHR_OK;
+  }
+  DeviceGuard g(device);
+  const Plan& P = ctx->plan;
+  cudaError_t e = cudaMalloc(&ctx->twid, P.twid.size() * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->twid, P.twid.data(), P.twid.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->cvec, P.cvec.size() * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->cvec, P.cvec.data(), P.cvec.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(ctx->twid);
+    cudaFree(ctx->cvec);
+    delete ctx;
+    return cuda_fail(e, "ctx create");
+  }
+  *out = ctx;
+  return SFHR_OK;
+}
+
+int sfhr_ctx_destroy(sfhr_ctx* ctx) {
+  if (!ctx) return SFHR_OK;
+  if (ctx->device < 0) {
+    delete ctx;
+    return SFHR_OK;
+  }
+  DeviceGuard g(ctx->device);
+  cudaFree(ctx->twid);
+  cudaFree(ctx->cvec);
+  delete ctx;
+  return SFHR_OK;
+}
+
+int sfhr_ctx_info(const sfhr_ctx* ctx, int64_t* info, int n) {
+  if (!ctx || !info) return -1;
+  const Plan& P = ctx->plan;
+  std::vector<int64_t> v = {P.rc.M, P.rc.N, P.rc.n1, P.rc.np, P.pack_factor, P.beta, P.shrink,
+                            P.inv_m_mod_p, (int64_t)P.cu};
+  for (int i = 0; i < P.rc.np; ++i) v.push_back(P.rc.pc[i].p);
+  v.push_back((int64_t)(P.bound_bits * 1000));
+  v.push_back((int64_t)(P.crt_bits * 1000));
+  int k = std::min<int>(n, (int)v.size());
+  for (int i = 0; i < k; ++i) info[i] = v[i];
+  return k;
+}
+
+int sfhr_ctx_debug_tables(const sfhr_ctx* ctx, void* ringconst, size_t rc_bytes, uint32_t* twid,
+                          size_t twid_words) {
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  const Plan& P = ctx->plan;
+  if (rc_bytes != sizeof(RingConst)) return fail(SFHR_EINVAL, "RingConst size mismatch");
+  std::memcpy(ringconst, &P.rc, sizeof(RingConst));
+  if (twid) std::memcpy(twid, P.twid.data(), std::min(twid_words, P.twid.size()) * 4);
+  return SFHR_OK;
+}
+
+size_t sfhr_ringconst_bytes(void) { return sizeof(RingConst); }
+
+int sfhr_ctx_dual(const sfhr_ctx* ctx, int32_t* e1, int32_t* e2, int32_t* ratio_len) {
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  const Plan& P = ctx->plan;
+  std::memcpy(e1, P.e1.data(), P.e1.size() * 4);
+  std::memcpy(e2, P.e2.data(), P.e2.size() * 4);
+  std::memcpy(ratio_len, P.cvec.data(), P.cvec.size() * 4);
+  return SFHR_OK;
+}
+
+int sfhr_register_ksk(sfhr_ctx* ctx, const uint32_t* idx, int nidx, const uint64_t* ksk, void* stream,
+                      sfhr_key** out) {
+  if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
+  if (!ctx || !out || (nidx > 0 && (!idx || !ksk))) return fail(SFHR_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  const Plan& P = ctx->plan;
+  const RingConst& rc = P.rc;
+  sfhr_key* key = new (std::nothrow) sfhr_key();
+  if (!key) return fail(SFHR_ENOMEM, "out of host memory");
+  key->ctx = ctx;
+  for (int s = 0; s < nidx; ++s) {
+    const uint32_t d = idx[s] % (uint32_t)rc.M;
+    if (std::gcd((long long)d, (long long)rc.M) != 1) {
+      delete key;
+      return fail(SFHR_EINVAL, "key-switch index " + std::to_string(d) + " not coprime with M");
+    }
+    key->slot[d] = s;
+  }
+  key->slot_words = (size_t)rc.l * 2 * rc.np * rc.N;
+  const size_t bytes = (size_t)std::max(nidx, 1) * key->slot_words * 4;
+  cudaError_t e = cudaMalloc(&key->spectra, bytes);
+  if (e != cudaSuccess) {
+    delete key;
+    return cuda_fail(e, "ksk spectra alloc");
+  }
+  SpecArgs a;
+  a.keys = ksk;
+  a.out = key->spectra;
+  a.twid = ctx->twid;
+  e = launch_spectra(rc, a, nidx * rc.l * 2, (cudaStream_t)stream);
+  if (e != cudaSuccess) {
+    cudaFree(key->spectra);
+    delete key;
+    return cuda_fail(e, "ksk spectra kernel");
+  }
+  *out = key;
+  return SFHR_OK;
+}
+
+int sfhr_key_destroy(sfhr_key* key) {
+  if (!key) return SFHR_OK;
+  DeviceGuard g(key->ctx->device);
+  cudaFree(key->spectra);
+  delete key;
+  return SFHR_OK;
+}
+
+int sfhr_automorphism_batch(sfhr_ctx* ctx, uint32_t d, const uint64_t* in, uint64_t* out, int64_t B,
+                            void* stream) {
+  if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  uint32_t dinv;
+  try {
+    dinv = inv_mod_M(ctx->plan, d);
+  } catch (const std::exception& ex) {
+    return fail(SFHR_EINVAL, ex.what());
+  }
+  CK(launch_automorphism(ctx->plan.rc, dinv, in, out, B, (cudaStream_t)stream), "automorphism kernel");
+  return SFHR_OK;
+}
+
+int sfhr_keyswitch_batch(sfhr_ctx* ctx, const sfhr_key* key, uint32_t d, const uint64_t* in, uint64_t* out,
+                         int64_t B, int skip_zero, unsigned long long* counter, void* stream) {
+  if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
+  if (!ctx || !key) return fail(SFHR_EINVAL, "null argument");
+  if (in == out) return fail(SFHR_EINVAL, "in and out must not alias");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  uint32_t reps[1] = {d};
+  return run_stage(ctx, key, reps, 1, 0, in, out, B, skip_zero, counter, (cudaStream_t)stream);
+}
+
+int sfhr_stage_batch(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nreps, const uint64_t* in,
+                     uint64_t* out, int64_t B, int skip_zero, unsigned long long* counter, void* stream) {
+  if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
+  if (!ctx || !key || !reps || nreps < 1) return fail(SFHR_EINVAL, "bad argument");
+  if (in == out) return fail(SFHR_EINVAL, "in and out must not alias");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  try {
+    return run_stage(ctx, key, reps, nreps, 1, in, out, B, skip_zero, counter, (cudaStream_t)stream);
+  } catch (const std::exception& ex) {
+    return fail(SFHR_EINVAL, ex.what());
+  }
+}
+
+int sfhr_extract(sfhr_ctx* ctx, const uint64_t* power, const uint32_t* exps, int npow, int k_chunks, int64_t E,
+                 uint64_t* rows, void* stream) {
+  if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  const Plan& P = ctx->plan;
+  if (E < 0 || E > (int64_t)k_chunks * P.rc.N) return fail(SFHR_EINVAL, "row count exceeds chunk capacity");
+  if (npow < 1 || npow > 64) return fail(SFHR_EINVAL, "bad power count");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  ExtractArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.power = power;
+  for (int q = 0; q < npow; ++q) a.exps[q] = exps[q] % (uint32_t)P.rc.M;
+  a.cvec = ctx->cvec;
+  a.rows = rows;
+  a.E = E;
+  a.k_chunks = k_chunks;
+  a.npow = npow;
+  a.cu = P.cu;
+  CK(launch_extract(P.rc, a, (cudaStream_t)stream), "extract kernel");
+  return SFHR_OK;
+}
+
+int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* d, void* stream) {
+  if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
+  if (!ctx || !d) return fail(SFHR_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  LinearArgs a;
+  a.in = d->in;
+  a.in_map = d->in_map;
+  a.round_in = d->round_in;
+  a.round_map = d->round_map;
+  a.out = d->out;
+  a.out_map = d->out_map;
+  a.groups = d->groups;
+  a.cols = d->cols;
+  a.weights = d->weights;
+  a.rows = d->rows;
+  a.ex_ptr = d->ex_ptr;
+  a.ex_col = d->ex_col;
+  a.ex_w = d->ex_w;
+  a.bias = d->bias;
+  a.unit = d->unit;
+  a.G = d->n_groups;
+  a.lanes = d->lanes ? d->lanes : 2 * (int64_t)ctx->plan.rc.N;
+  a.body_off = d->lanes ? d->body_off : ctx->plan.rc.N;
+  if (a.lanes > 65535LL * 128) return fail(SFHR_EINVAL, "too many lanes per row");
+  CK(launch_linear(ctx->plan.rc, a, (cudaStream_t)stream), "linear kernel");
+  return SFHR_OK;
+}
+
+size_t sfhr_pack_workspace_bytes(const sfhr_ctx* ctx, int64_t n_groups) {
+  if (!ctx) return 0;
+  return (size_t)n_groups * ctx->plan.pack_factor * 2 * ctx->plan.rc.N * 8;
+}
+
+int sfhr_pack(sfhr_ctx* ctx, const sfhr_key* key, uint64_t* rows, int64_t G, uint64_t* packs, void* ws,
+              size_t ws_bytes, int skip_zero, unsigned long long* counter, void* stream) {
+  if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
+  if (!ctx || !key) return fail(SFHR_EINVAL, "null argument");
+  if (G == 0) return SFHR_OK;
+  if (ws_bytes < sfhr_pack_workspace_bytes(ctx, G)) return fail(SFHR_EINVAL, "pack workspace too small");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  const Plan& P = ctx->plan;
+  const RingConst& rc = P.rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint64_t* cur = rows;
+  uint64_t* oth = (uint64_t*)ws;
+  int64_t per = P.pack_factor;  // rows per group at the current level
+  auto stage = [&](const std::vector<uint32_t>& reps) -> int {
+    int rc_ = run_stage(ctx, key, reps.data(), (int)reps.size(), 1, cur, oth, G * per, skip_zero, counter, st);
+    if (rc_ == SFHR_OK) std::swap(cur, oth);
+    return rc_;
+  };
+  const int t = rc.t, gamma = P.gamma, beta = P.beta;
+  try {
+    if (gamma == 0)
+      for (auto& ch : P.chains)
+        if (int e = stage(ch)) return e;
+    long long tj = 1;
+    for (int j = 1; j <= beta; ++j) {
+      tj *= t;
+      const int members = j == 1 ? t - 1 : t;
+      const int rest = (int)(per / members);
+      CK(launch_merge(rc, cur, oth, G, members, rest, (int)(rc.M / tj), st), "merge kernel");
+      std::swap(cur, oth);
+      per = rest;
+      if (j <= beta - 1 && j >= std::max(gamma, 1))
+        if (int e = stage(P.reps_above[j - 1])) return e;
+    }
+    for (int j = beta; j < rc.alpha; ++j)
+      if (j >= std::max(gamma, 1))
+        if (int e = stage(P.reps_above[j - 1])) return e;
+  } catch (const std::exception& ex) {
+    return fail(SFHR_EINVAL, ex.what());
+  }
+  CK(cudaMemcpyAsync(packs, cur, (size_t)G * 2 * rc.N * 8, cudaMemcpyDeviceToDevice, st), "pack copy");
+  return SFHR_OK;
+}
+
+int sfhr_derive_permutation(const uint8_t* seed, int seed_len, const uint8_t* sid, int sid_len, uint32_t round_no,
+                            int64_t size, int64_t* out) {
+  try {
+    derive_permutation(seed, seed_len, sid, sid_len, round_no, size, out);
+  } catch (const std::exception& ex) {
+    return fail(SFHR_EINVAL, ex.what());
+  }
+  return SFHR_OK;
+}
+
+}  // extern "C"

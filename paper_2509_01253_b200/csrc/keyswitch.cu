@@ -1,0 +1,503 @@
+// Fused hoisted key-switch stage kernel (sm_100a).
+//
+// Semantics (reference pkg/src/sfhr/tracepack.py:268-285 with
+// crypto.py:288-323, 400-464): for each input row x = (a, b) and the stage's
+// switched representatives r_1..r_T (automorphism index d_r, key set K_r):
+//
+//   y_r          = aut_{d_r}(x)                          (ring.py:101-130)
+//   dig_{r,i}    = balanced base-D digit i of y_r.a       (crypto.py:288-323)
+//   A            = sum_r sum_i dig_{r,i} * K_r[i].a  mod Phi_M
+//   B            = sum_r sum_i dig_{r,i} * K_r[i].b  mod Phi_M
+//   out.a        = [identity] * x.a - A                  (mod 2^53)
+//   out.b        = [identity] * x.b + sum_r y_r.b - B    (mod 2^53)
+//
+// which is acc = x + sum_r KS_r(aut_r(x)) for a stage, and the plain
+// switch_batch (one rep, d_r = 1, no identity term) otherwise.
+//
+// Device design: one thread-block CLUSTER per row, one CTA per CRT prime.
+// Each CTA stages x.a in shared memory, and for every rep computes the
+// automorphism gather + digit decomposition on the fly inside the first
+// transform step, runs the l digit Phi_M-NTTs together (one barrier per
+// radix-t stage), and multiply-accumulates the last butterfly outputs into
+// per-thread 64-bit register accumulators against the precomputed key
+// spectra (thread-owned layout => coalesced).  The reps are summed in the
+// NTT domain, so only 2 inverse transforms per prime per row are needed.
+// Finally the CTAs of the cluster exchange their residues through
+// distributed shared memory and each reconstructs a 1/NP slice of the row by
+// explicit CRT mod 2^53.
+#include <cooperative_groups.h>
+
+#include "sfhr_common.cuh"
+#include "sfhr_kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace sfhr {
+
+// ---------------------------------------------------------------------------
+// small DFT helpers (constants come from the __grid_constant__ parameter
+// block with compile-time offsets -> constant-bank operands)
+
+template <int T>
+__device__ __forceinline__ void dft_t(const uint32_t (&x)[T], uint32_t (&y)[T],
+                                      const uint32_t (&Z)[MAXT][MAXT], uint32_t p, uint32_t pinv) {
+#pragma unroll
+  for (int k = 0; k < T; ++k) {
+    uint64_t s = 0;
+#pragma unroll
+    for (int m = 0; m < T; ++m) s += (uint64_t)x[m] * Z[k][m];
+    y[k] = redc(s, p, pinv);
+  }
+}
+
+// balanced base-D decomposition of y < 2^53 into L signed digits
+template <int L>
+__device__ __forceinline__ void decompose(uint64_t y, int (&dg)[L], const RingConst& rc) {
+  if (rc.dlog2 >= 0) {
+    const int w = rc.dlog2;
+    const int D = rc.D;
+    uint64_t u = (y + (1ull << (rc.shift - 1))) >> rc.shift;
+    int raw[L];
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) {
+      raw[i] = (int)(u & (uint64_t)(D - 1));
+      u >>= w;
+    }
+    int carry = 0;
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) {
+      int x = raw[i] + carry;
+      int over = x > (D >> 1);
+      dg[i] = over ? x - D : x;
+      carry = over;
+    }
+  } else {
+    const long long D = rc.D;
+    long long r = (long long)y;
+    if (y > (1ull << 52)) r -= (1ll << 53);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      long long prod = r * D;
+      long long d = (prod + (1ll << 52)) >> 53;
+      dg[i] = (int)d;
+      r = prod - d * (1ll << 53);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t lift_signed(int d, uint32_t p) {
+  return d < 0 ? (uint32_t)(d + (int)p) : (uint32_t)d;
+}
+
+// ---------------------------------------------------------------------------
+// radix-T cyclic stages shared by the forward/inverse transforms
+
+// forward DIF stages s = 0 .. alpha-3 (all but the last, L > 1) on nb buffers
+template <int T, int PR>
+__device__ void fwd_mid_stages(uint32_t* buf, int nb, const RingConst& rc, const uint32_t* wt) {
+  const PrimeConst& pc = rc.pc[PR];
+  const int n1 = rc.n1, nsub = n1 / T;
+  int L = nsub;
+  for (int s = 0; s < rc.alpha - 2; ++s, L /= T) {
+    const int step = rc.M / (T * L);
+    for (int it = threadIdx.x; it < rc.nitems; it += blockDim.x) {
+      const int sub = it / nsub, rem = it - sub * nsub;
+      const int b = rem / L, j = rem - b * L;
+      const int base = sub * n1 + b * T * L + j;
+      const int e1 = step * j;
+      for (int q = 0; q < nb; ++q) {
+        uint32_t* v = buf + q * rc.N + base;
+        uint32_t x[T], y[T];
+#pragma unroll
+        for (int m = 0; m < T; ++m) x[m] = v[m * L];
+        dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
+        v[0] = y[0];
+#pragma unroll
+        for (int k = 1; k < T; ++k) v[k * L] = mont_mul(y[k], wt[e1 * k], pc.p, pc.pinv);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// inverse DIT stages s = alpha-3 .. 0 (all but the first-undone L == 1 stage)
+template <int T, int PR>
+__device__ void inv_mid_stages(uint32_t* buf, int nb, const RingConst& rc, const uint32_t* wt) {
+  const PrimeConst& pc = rc.pc[PR];
+  const int n1 = rc.n1, nsub = n1 / T;
+  int L = T;
+  for (int s = rc.alpha - 3; s >= 0; --s, L *= T) {
+    const int step = rc.M / (T * L);
+    for (int it = threadIdx.x; it < rc.nitems; it += blockDim.x) {
+      const int sub = it / nsub, rem = it - sub * nsub;
+      const int b = rem / L, j = rem - b * L;
+      const int base = sub * n1 + b * T * L + j;
+      const int e1 = step * j;
+      for (int q = 0; q < nb; ++q) {
+        uint32_t* v = buf + q * rc.N + base;
+        uint32_t z[T], x[T];
+        z[0] = v[0];
+#pragma unroll
+        for (int k = 1; k < T; ++k) z[k] = mont_mul(v[k * L], wt[rc.M - e1 * k], pc.p, pc.pinv);
+        dft_t<T>(z, x, pc.zi, pc.p, pc.pinv);
+#pragma unroll
+        for (int m = 0; m < T; ++m) v[m * L] = x[m];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// inverse first step: untwist + (t-1)x(t-1) solve, writes y_i in [0, p)
+template <int T, int PR>
+__device__ void inv_first_step(uint32_t* buf, int nb, const RingConst& rc, const uint32_t* wt) {
+  const PrimeConst& pc = rc.pc[PR];
+  const int n1 = rc.n1;
+  for (int m = threadIdx.x; m < n1; m += blockDim.x) {
+    for (int q = 0; q < nb; ++q) {
+      uint32_t* v = buf + q * rc.N + m;
+      uint32_t C[T - 1];
+#pragma unroll
+      for (int r = 1; r < T; ++r) C[r - 1] = mont_mul(v[(r - 1) * n1], wt[rc.M - r * m], pc.p, pc.pinv);
+#pragma unroll
+      for (int j = 0; j < T - 1; ++j) {
+        uint64_t s = 0;
+#pragma unroll
+        for (int r = 0; r < T - 1; ++r) s += (uint64_t)C[r] * pc.g[j][r];
+        v[j * n1] = fully(redc(s, pc.p, pc.pinv), pc.p);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// the fused stage kernel
+
+struct SmemLayout {
+  uint64_t* xa;
+  uint32_t* wt;
+  uint32_t* buf;
+};
+
+__device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst& rc, int nbuf) {
+  SmemLayout s;
+  s.xa = reinterpret_cast<uint64_t*>(smem);
+  s.wt = reinterpret_cast<uint32_t*>(smem + (size_t)rc.N * 8);
+  s.buf = s.wt + ((rc.M + 1 + 3) & ~3);
+  (void)nbuf;
+  return s;
+}
+
+template <int T, int L, int PR>
+__device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem) {
+  const PrimeConst& pc = rc.pc[PR];
+  const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
+  const int N = rc.N, n1 = rc.n1, M = rc.M;
+  const int nb = L > 2 ? L : 2;
+  SmemLayout S = carve(smem, rc, nb);
+  const int64_t row = blockIdx.x / rc.np;
+  const uint64_t* xin = a.in + row * 2 * (int64_t)N;
+  uint64_t* xout = a.out + row * 2 * (int64_t)N;
+  cg::cluster_group cluster = cg::this_cluster();
+
+  // stage x.a and the twiddle table; detect an all-zero row
+  int nz = 0;
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    uint64_t va = xin[k], vb = xin[N + k];
+    S.xa[k] = va;
+    nz |= (va | vb) != 0;
+  }
+  const uint32_t* wsrc = a.twid + (size_t)PR * (M + 1);
+  for (int k = threadIdx.x; k <= M; k += blockDim.x) S.wt[k] = wsrc[k];
+  const int live = __syncthreads_or(nz);
+  const int per = (N + rc.np - 1) / rc.np;
+  const int k0 = PR * per, k1 = min(N, k0 + per);
+  if (!live) {
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      xout[k] = 0;
+      xout[N + k] = 0;
+    }
+    if (PR == 0 && threadIdx.x == 0 && a.counter && !a.skip_zero)
+      atomicAdd(a.counter, (unsigned long long)a.nreps);
+    return;  // uniform across the cluster: every CTA saw the same row
+  }
+  if (PR == 0 && threadIdx.x == 0 && a.counter) atomicAdd(a.counter, (unsigned long long)a.nreps);
+
+  const int item = threadIdx.x;
+  const bool owner = item < rc.nitems;
+  uint64_t accA[T], accB[T];
+#pragma unroll
+  for (int k = 0; k < T; ++k) accA[k] = accB[k] = 0;
+
+  for (int r = 0; r < a.nreps; ++r) {
+    const uint32_t dinv = a.dinv[r];
+    const uint32_t step1 = fastmod((uint32_t)n1 * dinv, M, rc.magicM);
+    // ---- forward first step with fused automorphism + decomposition ----
+    for (int m = threadIdx.x; m < n1; m += blockDim.x) {
+      uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
+      const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
+      uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
+      int dg[L][T - 1];
+#pragma unroll
+      for (int j = 0; j < T - 1; ++j) {
+        const uint64_t v1 = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
+        int d[L];
+        decompose<L>((v1 - v2) & QMASK, d, rc);
+#pragma unroll
+        for (int i = 0; i < L; ++i) dg[i][j] = d[i];
+        s1 += step1;
+        if (s1 >= (uint32_t)M) s1 -= M;
+      }
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        uint32_t vals[T - 1];
+#pragma unroll
+        for (int j = 0; j < T - 1; ++j) vals[j] = lift_signed(dg[i][j], p);
+        uint32_t* o = S.buf + i * N + m;
+#pragma unroll
+        for (int q = 1; q < T; ++q) {
+          uint64_t s = 0;
+#pragma unroll
+          for (int j = 0; j < T - 1; ++j) s += (uint64_t)vals[j] * pc.z[q][j];
+          o[(q - 1) * n1] = mont_mul(redc(s, p, pinv), S.wt[q * m], p, pinv);
+        }
+      }
+    }
+    __syncthreads();
+    fwd_mid_stages<T, PR>(S.buf, L, rc, S.wt);
+    // ---- last stage (span 1) in registers, MAC against the key spectra ----
+    if (owner) {
+      const uint32_t* ks = a.spec[r];
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        const uint32_t* v = S.buf + i * N + item * T;
+        uint32_t x[T], y[T];
+#pragma unroll
+        for (int m = 0; m < T; ++m) x[m] = v[m];
+        dft_t<T>(x, y, pc.z, p, pinv);
+        const uint32_t* ka = ks + ((size_t)(i * 2 + 0) * rc.np + PR) * N + item;
+        const uint32_t* kb = ks + ((size_t)(i * 2 + 1) * rc.np + PR) * N + item;
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+          accA[k] += (uint64_t)y[k] * __ldg(ka + k * rc.nitems);
+          accB[k] += (uint64_t)y[k] * __ldg(kb + k * rc.nitems);
+        }
+      }
+      if (a.shrink) {
+#pragma unroll
+        for (int k = 0; k < T; ++k) {
+          uint32_t ha = (uint32_t)(accA[k] >> 32), hb = (uint32_t)(accB[k] >> 32);
+          ha -= __umulhi(ha, mu) * p;
+          hb -= __umulhi(hb, mu) * p;
+          accA[k] = (uint64_t)ha * pc.rmod + (uint32_t)accA[k];
+          accB[k] = (uint64_t)hb * pc.rmod + (uint32_t)accB[k];
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- inverse transforms of the two accumulators (buffers 0: a, 1: b) ----
+  if (owner) {
+    uint32_t za[T], zb[T], xa[T], xb[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      za[k] = redc_wide(accA[k], p, pinv, mu);
+      zb[k] = redc_wide(accB[k], p, pinv, mu);
+    }
+    dft_t<T>(za, xa, pc.zi, p, pinv);
+    dft_t<T>(zb, xb, pc.zi, p, pinv);
+#pragma unroll
+    for (int m = 0; m < T; ++m) {
+      S.buf[item * T + m] = xa[m];
+      S.buf[N + item * T + m] = xb[m];
+    }
+  }
+  __syncthreads();
+  inv_mid_stages<T, PR>(S.buf, 2, rc, S.wt);
+  inv_first_step<T, PR>(S.buf, 2, rc, S.wt);
+
+  // ---- explicit CRT across the cluster through distributed shared memory ----
+  cluster.sync();
+  const uint32_t* ry[MAXNP];
+#pragma unroll
+  for (int i = 0; i < MAXNP; ++i)
+    ry[i] = i < rc.np ? cluster.map_shared_rank(S.buf, i) : nullptr;
+  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    uint64_t ua = 0, ub = 0;
+    double fa = 0.0, fb = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXNP; ++i) {
+      if (i < rc.np) {
+        const uint32_t ya = ry[i][k], yb = ry[i][N + k];
+        ua += (uint64_t)ya * rc.pc[i].q_mod64;
+        ub += (uint64_t)yb * rc.pc[i].q_mod64;
+        fa += (double)ya * rc.pc[i].inv_p;
+        fb += (double)yb * rc.pc[i].inv_p;
+      }
+    }
+    const uint64_t A = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
+    const uint64_t B = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
+    uint64_t bsum = a.identity ? xin[N + k] : 0ull;
+    const uint32_t kmod = fastmod((uint32_t)k, n1, rc.magicN1);
+    for (int r = 0; r < a.nreps; ++r) {
+      const uint32_t dinv = a.dinv[r];
+      const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
+      const uint32_t s2 = fastmod((uint32_t)(N + kmod) * dinv, M, rc.magicM);
+      uint64_t v = s1 < (uint32_t)N ? xin[N + s1] : 0ull;
+      if (s2 < (uint32_t)N) v -= xin[N + s2];
+      bsum += v;
+    }
+    xout[k] = ((a.identity ? S.xa[k] : 0ull) - A) & QMASK;
+    xout[N + k] = (bsum - B) & QMASK;
+  }
+  cluster.sync();
+}
+
+template <int T, int L>
+__global__ void __launch_bounds__(512) ks_stage_kernel(const __grid_constant__ RingConst rc,
+                                                       const __grid_constant__ StageArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const unsigned rank = cg::this_cluster().block_rank();
+  switch (rank) {
+    case 0: stage_body<T, L, 0>(rc, a, smem); break;
+    case 1: stage_body<T, L, 1>(rc, a, smem); break;
+    case 2: stage_body<T, L, 2>(rc, a, smem); break;
+    default: stage_body<T, L, 3>(rc, a, smem); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// key spectra precompute: forward transform of (centered) key polynomials,
+// times R, stored in the thread-owned layout [k * nitems + item].
+// One CTA per (slot, digit, comp, prime); not performance critical.
+
+template <int T, int PR>
+__device__ void spectra_body(const RingConst& rc, const SpecArgs a, unsigned char* smem, int job) {
+  const PrimeConst& pc = rc.pc[PR];
+  const int N = rc.N, n1 = rc.n1;
+  SmemLayout S = carve(smem, rc, 1);
+  const uint64_t* src = a.keys + (size_t)job * N;  // job = (slot*l + i)*2 + c
+  for (int k = threadIdx.x; k <= rc.M; k += blockDim.x) S.wt[k] = a.twid[(size_t)PR * (rc.M + 1) + k];
+  __syncthreads();
+  for (int m = threadIdx.x; m < n1; m += blockDim.x) {
+    uint32_t vals[T - 1];
+#pragma unroll
+    for (int j = 0; j < T - 1; ++j) {
+      uint64_t v = src[j * n1 + m] & QMASK;
+      long long c = (long long)v;
+      if (v >= (1ull << 52)) c -= (1ll << 53);
+      long long r = c % (long long)pc.p;
+      if (r < 0) r += pc.p;
+      vals[j] = (uint32_t)r;
+    }
+#pragma unroll
+    for (int q = 1; q < T; ++q) {
+      uint64_t s = 0;
+#pragma unroll
+      for (int j = 0; j < T - 1; ++j) s += (uint64_t)vals[j] * pc.z[q][j];
+      S.buf[(q - 1) * n1 + m] = mont_mul(redc(s, pc.p, pc.pinv), S.wt[q * m], pc.p, pc.pinv);
+    }
+  }
+  __syncthreads();
+  fwd_mid_stages<T, PR>(S.buf, 1, rc, S.wt);
+  for (int it = threadIdx.x; it < rc.nitems; it += blockDim.x) {
+    uint32_t x[T], y[T];
+#pragma unroll
+    for (int m = 0; m < T; ++m) x[m] = S.buf[it * T + m];
+    dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
+    uint32_t* dst = a.out + ((size_t)job * rc.np + PR) * N + it;
+#pragma unroll
+    for (int k = 0; k < T; ++k) dst[k * rc.nitems] = fully(mont_mul(y[k], pc.r2, pc.p, pc.pinv), pc.p);
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(512) ks_spectra_kernel(const __grid_constant__ RingConst rc,
+                                                         const __grid_constant__ SpecArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int job = blockIdx.x / rc.np;
+  const int pr = blockIdx.x % rc.np;
+  switch (pr) {
+    case 0: spectra_body<T, 0>(rc, a, smem, job); break;
+    case 1: spectra_body<T, 1>(rc, a, smem, job); break;
+    case 2: spectra_body<T, 2>(rc, a, smem, job); break;
+    default: spectra_body<T, 3>(rc, a, smem, job); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+size_t stage_smem_bytes(const RingConst& rc) {
+  const int nb = rc.l > 2 ? rc.l : 2;
+  return (size_t)rc.N * 8 + (size_t)((rc.M + 1 + 3) & ~3) * 4 + (size_t)nb * rc.N * 4;
+}
+
+int stage_threads(const RingConst& rc) { return ((rc.nitems + 31) / 32) * 32; }
+
+template <int T, int L>
+static cudaError_t launch_stage_tl(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
+  auto kern = ks_stage_kernel<T, L>;
+  const size_t smem = stage_smem_bytes(rc);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.B * rc.np), 1, 1);
+  cfg.blockDim = dim3(stage_threads(rc), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = rc.np;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, rc, a);
+}
+
+template <int T>
+static cudaError_t launch_stage_t(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
+  switch (rc.l) {
+    case 1: return launch_stage_tl<T, 1>(rc, a, st);
+    case 2: return launch_stage_tl<T, 2>(rc, a, st);
+    case 3: return launch_stage_tl<T, 3>(rc, a, st);
+    case 4: return launch_stage_tl<T, 4>(rc, a, st);
+    case 5: return launch_stage_tl<T, 5>(rc, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_stage(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
+  if (a.B == 0 || a.nreps == 0) return cudaSuccess;
+  switch (rc.t) {
+    case 3: return launch_stage_t<3>(rc, a, st);
+    case 5: return launch_stage_t<5>(rc, a, st);
+    case 7: return launch_stage_t<7>(rc, a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int T>
+static cudaError_t launch_spec_t(const RingConst& rc, const SpecArgs& a, int njobs, cudaStream_t st) {
+  auto kern = ks_spectra_kernel<T>;
+  const size_t smem = stage_smem_bytes(rc);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<njobs * rc.np, stage_threads(rc), smem, st>>>(rc, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spectra(const RingConst& rc, const SpecArgs& a, int njobs, cudaStream_t st) {
+  if (njobs == 0) return cudaSuccess;
+  switch (rc.t) {
+    case 3: return launch_spec_t<3>(rc, a, njobs, st);
+    case 5: return launch_spec_t<5>(rc, a, njobs, st);
+    case 7: return launch_spec_t<7>(rc, a, njobs, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace sfhr

@@ -1,0 +1,290 @@
+// Host-side planning for a ring row: NTT primes, Montgomery constants,
+// explicit-CRT constants, twiddle tables, the two-term dual basis, and the
+// tower/pack schedule.  Pure C++ (no CUDA calls).
+#include "plan.h"
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+namespace sfhr {
+
+static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) {
+  return (uint64_t)((unsigned __int128)a * b % m);
+}
+static uint64_t powmod(uint64_t a, uint64_t e, uint64_t m) {
+  uint64_t r = 1 % m;
+  a %= m;
+  while (e) {
+    if (e & 1) r = mulmod(r, a, m);
+    a = mulmod(a, a, m);
+    e >>= 1;
+  }
+  return r;
+}
+static bool is_prime_u32(uint64_t n) {
+  if (n < 2) return false;
+  for (uint64_t p : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull, 19ull, 23ull, 29ull, 31ull, 37ull})
+    if (n % p == 0) return n == p;
+  uint64_t d = n - 1;
+  int s = 0;
+  while (!(d & 1)) { d >>= 1; ++s; }
+  for (uint64_t a : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull}) {
+    uint64_t x = powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int r = 1; r < s; ++r) {
+      x = mulmod(x, x, n);
+      if (x == n - 1) { comp = false; break; }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+static bool small_prime(int n) {
+  if (n < 2) return false;
+  for (int k = 2; k * k <= n; ++k)
+    if (n % k == 0) return false;
+  return true;
+}
+static std::vector<int> factor_multiset(int n) {
+  std::vector<int> f;
+  for (int k = 2; k * k <= n; ++k)
+    while (n % k == 0) { f.push_back(k); n /= k; }
+  if (n > 1) f.push_back(n);
+  return f;
+}
+static int primitive_root_small(int t) {
+  auto fs = factor_multiset(t - 1);
+  for (int g = 2; g < t; ++g) {
+    bool ok = true;
+    for (int f : fs)
+      if (powmod(g, (t - 1) / f, t) == 1) { ok = false; break; }
+    if (ok) return g;
+  }
+  throw std::invalid_argument("no primitive root");
+}
+static uint64_t inv_mod(uint64_t a, uint64_t m) {  // m prime
+  return powmod(a, m - 2, m);
+}
+static int64_t inv_mod_any(int64_t a, int64_t m) {  // gcd(a, m) = 1
+  int64_t g = m, x = 0, x1 = 1, aa = ((a % m) + m) % m;
+  while (aa) {
+    int64_t q = g / aa;
+    int64_t t = g - q * aa; g = aa; aa = t;
+    t = x - q * x1; x = x1; x1 = t;
+  }
+  return ((x % m) + m) % m;
+}
+
+// Tr(zeta_M^k) over Q (reference dual.py:18-27)
+static long long tr_zeta(long long k, int t, int alpha) {
+  long long M = 1, n1 = 1;
+  for (int i = 0; i < alpha; ++i) M *= t;
+  n1 = M / t;
+  k %= M;
+  if (k < 0) k += M;
+  if (k == 0) return n1 * (t - 1);
+  return (k % n1 == 0) ? -n1 : 0;
+}
+
+Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) {
+  if (t < 3 || !small_prime(t)) throw std::invalid_argument("t must be an odd prime >= 3");
+  if (t != 3 && t != 5 && t != 7) throw std::invalid_argument("device kernels support t in {3, 5, 7}");
+  if (alpha < 2) throw std::invalid_argument("device kernels need alpha >= 2");
+  if (p_bits < 8 || p_bits > 16) throw std::invalid_argument("p must be a power of two between 2^8 and 2^16");
+  if (D < 2 || l < 1) throw std::invalid_argument("need D >= 2 and l >= 1");
+  if (l > MAXL) throw std::invalid_argument("gadget depth l > 5 unsupported on device");
+  if (gamma < 0 || gamma > 2) throw std::invalid_argument("extraction level gamma must be 0, 1 or 2");
+  const int beta_eff = beta ? beta : alpha - 1;
+  if (beta_eff < 1 || beta_eff > alpha - 1)
+    throw std::invalid_argument("packing level beta must satisfy 1 <= beta <= alpha-1");
+
+  Plan P;
+  RingConst& rc = P.rc;
+  std::memset(&rc, 0, sizeof(rc));
+  rc.t = t;
+  rc.alpha = alpha;
+  long long M = 1;
+  for (int i = 0; i < alpha; ++i) M *= t;
+  rc.M = (int)M;
+  rc.n1 = (int)(M / t);
+  rc.N = rc.n1 * (t - 1);
+  rc.nitems = rc.N / t;
+  rc.l = l;
+  rc.D = D;
+  // D^l <= q
+  {
+    long double lg = l * std::log2((long double)D);
+    if (lg > 53.0L + 1e-12L) throw std::invalid_argument("D^l must not exceed q");
+  }
+  if ((D & (D - 1)) == 0) {
+    int w = 0;
+    while ((1 << w) < D) ++w;
+    rc.dlog2 = w;
+    rc.shift = 53 - w * l;
+    if (rc.shift < 1) throw std::invalid_argument("gadget with D^l == q unsupported");
+  } else {
+    if (D > 1024) throw std::invalid_argument("non-power-of-two base must be <= 1024");
+    rc.dlog2 = -1;
+    rc.shift = 0;
+  }
+  if (rc.nitems > 1024) throw std::invalid_argument("ring too large for one CTA per row (N/t > 1024)");
+  rc.magicM = (uint32_t)((1ull << 32) / (uint64_t)rc.M);
+  rc.magicN1 = (uint32_t)((1ull << 32) / (uint64_t)rc.n1);
+
+  P.p_bits = p_bits;
+  P.gamma = gamma;
+  P.beta = beta_eff;
+  P.pack_factor = 1;
+  for (int i = 0; i < beta_eff - 1; ++i) P.pack_factor *= t;
+  P.pack_factor *= (t - 1);
+
+  // ---- schedule (reference tracepack.py:179-201, 288-326) ----
+  {
+    int g = primitive_root_small(t);
+    long long stride = 1;
+    for (int ell : factor_multiset(t - 1)) {
+      std::vector<uint32_t> ch;
+      for (int u = 0; u < ell; ++u) ch.push_back((uint32_t)powmod(g, stride * u, M));
+      P.chains.push_back(ch);
+      stride *= ell;
+    }
+    for (int j = 1; j < alpha; ++j) {
+      std::vector<uint32_t> reps;
+      long long tj = 1;
+      for (int i = 0; i < j; ++i) tj *= t;
+      for (int i = 0; i < t; ++i) reps.push_back((uint32_t)((1 + i * tj) % M));
+      P.reps_above.push_back(reps);
+    }
+  }
+  int maxreps = t - 1;
+  for (auto& ch : P.chains) maxreps = std::max(maxreps, (int)ch.size() - 1);
+  if (maxreps > MAXREPS) throw std::invalid_argument("too many representatives per stage");
+
+  // ---- NTT primes: p = 1 mod M, p < 2^31 / max(t, l) ----
+  const uint64_t limit = ((1ull << 31) - 1) / (uint64_t)std::max(t, l);
+  // worst-case |coefficient| of one stage's NTT-domain sum, centered keys:
+  //   maxreps * 2 (fold) * l * N * ceil(D/2) * 2^52
+  const long double bound_bits = std::log2((long double)maxreps * 2.0L * l * rc.N *
+                                           (long double)((D + 1) / 2)) + 52.0L;
+  std::vector<uint64_t> primes;
+  long double pbits = 0;
+  for (uint64_t k = (limit - 1) / (uint64_t)M; k > 0 && (int)primes.size() < MAXNP; --k) {
+    uint64_t p = k * (uint64_t)M + 1;
+    if (p >= limit || !is_prime_u32(p)) continue;
+    primes.push_back(p);
+    pbits += std::log2((long double)p);
+    if (pbits >= bound_bits + 1.5L) break;
+  }
+  if (pbits < bound_bits + 1.5L) throw std::invalid_argument("no CRT prime set large enough for this gadget");
+  rc.np = (int)primes.size();
+  P.bound_bits = (double)bound_bits;
+  P.crt_bits = (double)pbits;
+  // accumulator headroom: maxreps * l products of (< 2p) * (< p) must stay < 2^63
+  {
+    long double pm = (long double)primes[0];
+    long double tot = (long double)maxreps * l * 2.0L * pm * pm;
+    P.shrink = tot >= 9.2e18L ? 1 : 0;
+  }
+
+  uint64_t Pmod = 1;
+  for (uint64_t p : primes) Pmod *= p;
+  rc.P_mod64 = Pmod;
+  P.twid.assign((size_t)rc.np * (M + 1), 0);
+  const uint64_t R32 = 1ull << 32;
+  for (int i = 0; i < rc.np; ++i) {
+    const uint64_t p = primes[i];
+    PrimeConst& pc = rc.pc[i];
+    pc.p = (uint32_t)p;
+    uint32_t inv = 1;
+    for (int it = 0; it < 5; ++it) inv *= 2u - (uint32_t)p * inv;  // Newton: p^-1 mod 2^32
+    pc.pinv = inv;
+    pc.mu = (uint32_t)(R32 / p);
+    pc.rmod = (uint32_t)(R32 % p);
+    pc.r2 = (uint32_t)mulmod(R32 % p, R32 % p, p);
+    uint64_t omega = 0;
+    for (uint64_t x = 2; x < p; ++x) {
+      uint64_t w = powmod(x, (p - 1) / M, p);
+      if (powmod(w, M / t, p) != 1) { omega = w; break; }
+    }
+    if (!omega) throw std::runtime_error("no primitive M-th root");
+    const uint64_t Rm = R32 % p;
+    auto mont = [&](uint64_t v) { return (uint32_t)mulmod(v % p, Rm, p); };
+    const uint64_t zeta = powmod(omega, M / t, p);
+    for (int k = 0; k < t; ++k)
+      for (int m = 0; m < t; ++m) {
+        pc.z[k][m] = mont(powmod(zeta, (uint64_t)((k * m) % t), p));
+        pc.zi[k][m] = mont(powmod(zeta, (uint64_t)((t - (k * m) % t) % t), p));
+      }
+    // CRT: Q_i = P / p_i, Qinv = Q_i^-1 mod p_i
+    uint64_t qmod64 = 1, qmodp = 1;
+    for (int j = 0; j < rc.np; ++j)
+      if (j != i) {
+        qmod64 *= primes[j];
+        qmodp = mulmod(qmodp, primes[j] % p, p);
+      }
+    pc.q_mod64 = qmod64;
+    pc.inv_p = 1.0 / (double)p;
+    const uint64_t qinv = inv_mod(qmodp, p);
+    const uint64_t minv = inv_mod((uint64_t)M % p, p);
+    for (int j = 0; j < t - 1; ++j)
+      for (int r = 1; r < t; ++r) {
+        uint64_t a = powmod(zeta, (uint64_t)((t - (r * j) % t) % t), p);
+        uint64_t b = powmod(zeta, (uint64_t)(r % t), p);
+        uint64_t v = (a + p - b) % p;
+        v = mulmod(mulmod(v, minv, p), qinv, p);
+        pc.g[j][r - 1] = mont(v);
+      }
+    uint64_t w = 1;
+    for (long long e = 0; e <= M; ++e) {
+      P.twid[(size_t)i * (M + 1) + e] = mont(e == M ? 1 : w);
+      w = mulmod(w, omega, p);
+    }
+  }
+
+  // ---- dual basis two-term forms (reference dual.py:108-166) ----
+  P.e1.assign(rc.N, 0);
+  P.e2.assign(rc.N, 0);
+  P.cvec.assign(rc.N, 0);
+  const int n1 = rc.n1, N = rc.N;
+  for (int i = 0; i < N; ++i) {
+    const long long a = (M - i) % M;
+    const int first = i / n1 + 1;
+    bool found = false;
+    std::vector<int> cands = {first};
+    for (int c = 1; c < t; ++c)
+      if (c != first) cands.push_back(c);
+    for (int c : cands) {
+      const long long b = (a + (long long)c * n1) % M;
+      bool ok = true;
+      for (int j = i % n1; j < N && ok; j += n1) {
+        long long pr = tr_zeta(j + a, t, alpha) - tr_zeta(j + b, t, alpha);
+        ok = pr == (j == i ? M : 0);
+      }
+      if (ok) {
+        P.e1[i] = (int32_t)a;
+        P.e2[i] = (int32_t)b;
+        P.cvec[i] = c;
+        found = true;
+        break;
+      }
+    }
+    if (!found) throw std::runtime_error("dual basis index has no two-term form");
+  }
+  const long long pmod = 1ll << p_bits;
+  long long u = inv_mod_any(M % pmod, pmod);
+  P.inv_m_mod_p = u;
+  const long long cu = u > pmod / 2 ? u - pmod : u;
+  P.cu = (uint64_t)(int64_t)cu;
+  return P;
+}
+
+uint32_t inv_mod_M(const Plan& P, uint32_t d) {
+  const long long M = P.rc.M;
+  if (std::gcd((long long)d % M, M) != 1) throw std::invalid_argument("automorphism index not coprime with M");
+  return (uint32_t)inv_mod_any((long long)d % M, M);
+}
+
+}  // namespace sfhr

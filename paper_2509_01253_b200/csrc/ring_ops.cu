@@ -1,0 +1,204 @@
+// Gather-style ring kernels: automorphism, tower merge, partial extraction,
+// and the grouped ciphertext x plaintext linear map.  All are HBM/L2-bound
+// integer kernels: coalesced along the coefficient axis, one 64-bit lane per
+// thread, mod-2^53 wrap arithmetic.
+#include "sfhr_common.cuh"
+#include "sfhr_kernels.h"
+
+namespace sfhr {
+
+// ---------------------------------------------------------------------------
+// automorphism + fold: out[k] = v[s1]*[s1<N] - v[s2]*[s2<N]
+// with s1 = k*d^-1, s2 = (N + k mod n1)*d^-1 (mod M)   (reference ring.py:101-130)
+
+__global__ void automorphism_kernel(const __grid_constant__ RingConst rc, uint32_t dinv,
+                                    const uint64_t* __restrict__ in, uint64_t* __restrict__ out) {
+  const int64_t rc_row = blockIdx.x;  // (b, comp)
+  const uint64_t* v = in + rc_row * rc.N;
+  uint64_t* o = out + rc_row * rc.N;
+  for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < rc.N; k += gridDim.y * blockDim.x) {
+    const uint32_t km = fastmod((uint32_t)k, rc.n1, rc.magicN1);
+    const uint32_t s1 = fastmod((uint32_t)k * dinv, rc.M, rc.magicM);
+    const uint32_t s2 = fastmod((uint32_t)(rc.N + km) * dinv, rc.M, rc.magicM);
+    uint64_t r = s1 < (uint32_t)rc.N ? v[s1] : 0ull;
+    if (s2 < (uint32_t)rc.N) r -= v[s2];
+    o[k] = r & QMASK;
+  }
+}
+
+cudaError_t launch_automorphism(const RingConst& rc, uint32_t dinv, const uint64_t* in,
+                                uint64_t* out, int64_t B, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  dim3 grid((unsigned)(B * 2), (rc.N + 255) / 256);
+  automorphism_kernel<<<grid, 256, 0, st>>>(rc, dinv, in, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// tower merge (reference tracepack.py:307-316 with ring.py:77-84)
+
+__global__ void merge_kernel(const __grid_constant__ RingConst rc, const uint64_t* __restrict__ in,
+                             uint64_t* __restrict__ out, int members, int rest, int stride) {
+  const int64_t orow = blockIdx.x;          // (g, r)
+  const int comp = blockIdx.z;
+  const int64_t g = orow / rest;
+  const int r = (int)(orow - g * rest);
+  const int N = rc.N, M = rc.M;
+  for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < N; k += gridDim.y * blockDim.x) {
+    const int km = (int)fastmod((uint32_t)k, rc.n1, rc.magicN1);
+    uint64_t acc = 0;
+    for (int a = 0; a < members; ++a) {
+      const uint64_t* v = in + ((g * members + a) * (int64_t)rest + r) * 2 * N + (int64_t)comp * N;
+      const int e = (int)(((int64_t)a * stride) % M);
+      int s1 = k - e;
+      if (s1 < 0) s1 += M;
+      int s2 = N + km - e;
+      if (s2 < 0) s2 += M;
+      uint64_t t = s1 < N ? v[s1] : 0ull;
+      if (s2 < N) t -= v[s2];
+      acc += t;
+    }
+    out[orow * 2 * N + (int64_t)comp * N + k] = acc & QMASK;
+  }
+}
+
+cudaError_t launch_merge(const RingConst& rc, const uint64_t* in, uint64_t* out, int64_t G,
+                         int members, int rest, int stride, cudaStream_t st) {
+  if (G == 0) return cudaSuccess;
+  dim3 grid((unsigned)(G * rest), (rc.N + 255) / 256, 2);
+  merge_kernel<<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// partial-trace extraction (reference tracepack.py:118-154):
+//   row_i = fold( sum_d cu * (ct_d[x] - ct_d[x - c_i n1 d]) ),  x = (i d + m) mod M
+
+__global__ void extract_kernel(const __grid_constant__ RingConst rc, const __grid_constant__ ExtractArgs a) {
+  const int64_t g = blockIdx.x;
+  const int j = (int)(g / rc.N);
+  const int i = (int)(g - (int64_t)j * rc.N);
+  const int N = rc.N, M = rc.M, n1 = rc.n1;
+  const int ci = a.cvec[i];
+  for (int lane = blockIdx.y * blockDim.x + threadIdx.x; lane < 2 * N; lane += gridDim.y * blockDim.x) {
+    const int comp = lane >= N;
+    const int k = lane - comp * N;
+    const uint32_t km = fastmod((uint32_t)k, n1, rc.magicN1);
+    uint64_t acc = 0;
+    for (int q = 0; q < a.npow; ++q) {
+      const uint32_t d = a.exps[q];
+      const uint64_t* ct = a.power + (((int64_t)j * a.npow + q) * 2 + comp) * N;
+      const uint32_t id = fastmod((uint32_t)i * d, M, rc.magicM);
+      const uint32_t sh = fastmod((uint32_t)(ci * n1) * d, M, rc.magicM);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t x = id + (h ? (uint32_t)(N + km) : (uint32_t)k);
+        x = x >= (uint32_t)M ? x - M : x;
+        x = x >= (uint32_t)M ? x - M : x;
+        uint32_t y = x + M - sh;
+        y = y >= (uint32_t)M ? y - M : y;
+        uint64_t t = x < (uint32_t)N ? __ldg(ct + x) : 0ull;
+        if (y < (uint32_t)N) t -= __ldg(ct + y);
+        acc = h ? acc - t : acc + t;
+      }
+    }
+    a.rows[g * 2 * N + lane] = (acc * a.cu) & QMASK;
+  }
+}
+
+cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
+  if (a.E == 0) return cudaSuccess;
+  dim3 grid((unsigned)a.E, (2 * rc.N + 255) / 256);
+  extract_kernel<<<grid, 256, 0, st>>>(rc, a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// grouped linear map over ciphertext rows (reference model.py:384-429):
+// exact mod 2^53 via a 31/22-bit operand split: w*x = w*x_lo + (w*x_hi) 2^31,
+// the high product only matters mod 2^22, so a 32-bit accumulator suffices.
+
+constexpr int RPG = 16;  // rows per group
+
+__global__ void __launch_bounds__(128) linear_kernel(const __grid_constant__ RingConst rc,
+                                                     const __grid_constant__ LinearArgs a) {
+  const int64_t g = blockIdx.x;
+  const int64_t W2 = a.lanes;
+  const int64_t lane = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (lane >= W2) return;
+  const int32_t* gr = a.groups + 6 * g;
+  const int c0 = gr[0], nc = gr[1], w0 = gr[2], r0 = gr[3], nr = gr[4], per = gr[5];
+  uint64_t lo[RPG];
+  uint32_t hi[RPG];
+#pragma unroll
+  for (int r = 0; r < RPG; ++r) { lo[r] = 0; hi[r] = 0; }
+
+  if (!per) {
+    for (int c = 0; c < nc; ++c) {
+      const int col = __ldg(a.cols + c0 + c);
+      if (col < 0) continue;
+      const int64_t src = a.in_map ? __ldg(a.in_map + col) : col;
+      const uint64_t x = __ldg(a.in + src * W2 + lane);
+      const int64_t xl = (int64_t)(x & 0x7fffffffull);
+      const uint32_t xh = (uint32_t)(x >> 31);
+      const int4* wv = reinterpret_cast<const int4*>(a.weights + w0 + (int64_t)c * RPG);
+      int w[RPG];
+#pragma unroll
+      for (int q = 0; q < RPG / 4; ++q) {
+        const int4 v = __ldg(wv + q);
+        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int r = 0; r < RPG; ++r) {
+        lo[r] += (uint64_t)((int64_t)w[r] * xl);
+        hi[r] += (uint32_t)w[r] * xh;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < RPG; ++r) {
+      if (r < nr) {
+        for (int c = 0; c < nc; ++c) {
+          const int col = __ldg(a.cols + c0 + r * nc + c);
+          if (col < 0) continue;
+          const int64_t src = a.in_map ? __ldg(a.in_map + col) : col;
+          const uint64_t x = __ldg(a.in + src * W2 + lane);
+          const int wt = __ldg(a.weights + w0 + c * RPG + r);
+          lo[r] += (uint64_t)((int64_t)wt * (int64_t)(x & 0x7fffffffull));
+          hi[r] += (uint32_t)wt * (uint32_t)(x >> 31);
+        }
+      }
+    }
+  }
+
+#pragma unroll
+  for (int r = 0; r < RPG; ++r) {
+    if (r < nr) {
+      const int o = __ldg(a.rows + r0 + r);
+      if (a.ex_ptr) {
+        const int e0 = __ldg(a.ex_ptr + o), e1 = __ldg(a.ex_ptr + o + 1);
+        for (int e = e0; e < e1; ++e) {
+          const int col = __ldg(a.ex_col + e);
+          const int64_t src = a.round_map ? __ldg(a.round_map + col) : col;
+          const uint64_t x = __ldg(a.round_in + src * W2 + lane);
+          const int wt = __ldg(a.ex_w + e);
+          lo[r] += (uint64_t)((int64_t)wt * (int64_t)(x & 0x7fffffffull));
+          hi[r] += (uint32_t)wt * (uint32_t)(x >> 31);
+        }
+      }
+      uint64_t v = lo[r] + ((uint64_t)hi[r] << 31);
+      if (a.bias && lane >= a.body_off) v += (uint64_t)__ldg(a.bias + o) * __ldg(a.unit + (lane - a.body_off));
+      const int64_t dst = a.out_map ? __ldg(a.out_map + o) : o;
+      a.out[dst * W2 + lane] = v & QMASK;
+    }
+  }
+}
+
+cudaError_t launch_linear(const RingConst& rc, const LinearArgs& a, cudaStream_t st) {
+  if (a.G == 0) return cudaSuccess;
+  dim3 grid((unsigned)a.G, (unsigned)((a.lanes + 127) / 128));
+  linear_kernel<<<grid, 128, 0, st>>>(rc, a);
+  return cudaGetLastError();
+}
+
+}  // namespace sfhr

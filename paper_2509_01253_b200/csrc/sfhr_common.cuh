@@ -1,0 +1,79 @@
+// Shared definitions for the sm_100a Safhire server kernels.
+//
+// Ciphertext rows are (2, N) little-endian uint64 torus numerators mod
+// q = 2^53 (reference pkg/src/sfhr/params.py:14-16); every integer op on them
+// is uint64 wrap followed by & QMASK (reference ring.py:1-9).
+//
+// The key-switch convolution is done exactly over NP <= 4 word-size primes
+// p_i = 1 (mod M) (p_i < 2^31 / max(t, l)) with a "Phi_M-NTT": evaluation of
+// degree-<N polynomials at the N primitive M-th roots of unity, followed by
+// explicit CRT mod 2^53.  Arithmetic is 32-bit Montgomery with R = 2^32; data
+// is kept lazily in [0, 2p), constants fully reduced in [0, p).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sfhr {
+
+constexpr int MAXT = 7;     // largest supported ring prime t (3, 5, 7)
+constexpr int MAXNP = 4;    // CRT primes
+constexpr int MAXL = 5;     // gadget depth
+constexpr int MAXREPS = 8;  // switched automorphisms per stage (t-1 <= 6)
+constexpr uint64_t QMASK = (1ull << 53) - 1;
+
+struct PrimeConst {
+  uint32_t p;      // NTT prime, p = 1 mod M, p < 2^31 / max(t, l)
+  uint32_t pinv;   // p^-1 mod 2^32
+  uint32_t mu;     // floor(2^32 / p)
+  uint32_t r2;     // 2^64 mod p   (to enter Montgomery form)
+  uint32_t rmod;   // 2^32 mod p
+  uint32_t z[MAXT][MAXT];   // zeta^(k m) * R mod p, zeta = omega^(M/t)
+  uint32_t zi[MAXT][MAXT];  // zeta^(-k m) * R mod p
+  uint32_t g[MAXT][MAXT];   // inverse first step [j][r-1]: (zeta^(-rj) - zeta^r) / M * Qinv * R
+  uint64_t q_mod64;         // (P / p) mod 2^64
+  double inv_p;             // 1.0 / p
+};
+
+struct RingConst {
+  int t, alpha, M, N, n1, nitems;   // nitems = N / t
+  int np;                            // CRT primes in use
+  int l, D, dlog2, shift;            // gadget; dlog2 = -1 for odd D
+  uint32_t magicM;                   // floor(2^32 / M)
+  uint32_t magicN1;                  // floor(2^32 / n1)
+  uint64_t P_mod64;                  // prod p_i mod 2^64
+  PrimeConst pc[MAXNP];
+};
+
+#ifdef __CUDACC__
+// x < p * 2^32  ->  x * 2^-32 mod p, in (0, 2p)
+__device__ __forceinline__ uint32_t redc(uint64_t x, uint32_t p, uint32_t pinv) {
+  uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  uint32_t m = lo * pinv;
+  return hi - __umulhi(m, p) + p;
+}
+
+// x < 2^63  ->  x * 2^-32 mod p, in [0, 2p)
+__device__ __forceinline__ uint32_t redc_wide(uint64_t x, uint32_t p, uint32_t pinv, uint32_t mu) {
+  uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+  uint32_t m = lo * pinv;
+  uint32_t r = hi - __umulhi(m, p) + p;
+  return r - __umulhi(r, mu) * p;
+}
+
+// a in [0, 2p), bm = b*R mod p  ->  a*b mod p in (0, 2p)
+__device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t bm, uint32_t p, uint32_t pinv) {
+  return redc((uint64_t)a * bm, p, pinv);
+}
+
+// [0, 2p) -> [0, p)
+__device__ __forceinline__ uint32_t fully(uint32_t a, uint32_t p) { return a >= p ? a - p : a; }
+
+// x mod M for x < 2^32 using magic = floor(2^32 / M)
+__device__ __forceinline__ uint32_t fastmod(uint32_t x, uint32_t M, uint32_t magic) {
+  uint32_t r = x - __umulhi(x, magic) * M;
+  return r >= M ? r - M : r;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace sfhr

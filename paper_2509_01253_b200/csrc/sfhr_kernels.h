@@ -1,0 +1,79 @@
+// Internal kernel interfaces (not part of the public C-ABI; see include/sfhr_b200.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sfhr_common.cuh"
+
+namespace sfhr {
+
+struct StageArgs {
+  const uint64_t* in;     // (B, 2, N)
+  uint64_t* out;          // (B, 2, N), may not alias in
+  int64_t B;
+  int nreps;              // switched representatives (identity excluded)
+  int identity;           // 1: stage (acc = x + ...), 0: plain switch_batch
+  int skip_zero;          // zero rows are not counted
+  int shrink;             // reduce 64-bit accumulators after every rep
+  uint32_t dinv[MAXREPS]; // d^-1 mod M of each rep's automorphism (1 = none)
+  const uint32_t* spec[MAXREPS];  // key spectra of each rep: [l][2][np][N]
+  const uint32_t* twid;   // [np][M+1] omega^e * R mod p
+  unsigned long long* counter;    // live-row switch counter (may be null)
+};
+
+struct SpecArgs {
+  const uint64_t* keys;   // (jobs, N) key polynomials, job = (slot*l + i)*2 + c
+  uint32_t* out;          // (jobs, np, N) thread-owned layout
+  const uint32_t* twid;
+};
+
+size_t stage_smem_bytes(const RingConst& rc);
+int stage_threads(const RingConst& rc);
+cudaError_t launch_stage(const RingConst& rc, const StageArgs& a, cudaStream_t st);
+cudaError_t launch_spectra(const RingConst& rc, const SpecArgs& a, int njobs, cudaStream_t st);
+
+// ---- elementwise ring ops (ring_ops.cu) ----
+
+// out[b] = aut_d(in[b]) for (B, 2, N) batches (reference ring.py:124-130)
+cudaError_t launch_automorphism(const RingConst& rc, uint32_t dinv, const uint64_t* in,
+                                uint64_t* out, int64_t B, cudaStream_t st);
+
+// merge: out[g][r] = sum_a X^(a*stride) * in[g][a*rest + r]   (tracepack.py:307-316)
+cudaError_t launch_merge(const RingConst& rc, const uint64_t* in, uint64_t* out, int64_t G,
+                         int members, int rest, int stride, cudaStream_t st);
+
+struct ExtractArgs {
+  const uint64_t* power;   // (k_chunks, npow, 2, N) in ascending exponent order
+  uint32_t exps[64];       // (npow,) exponents
+  const int32_t* cvec;     // (N,) dual ratio_len c_i
+  uint64_t* rows;          // (E, 2, N), row j*N + i
+  int64_t E;
+  int k_chunks, npow;
+  uint64_t cu;             // centered M^-1 mod p as uint64
+};
+cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream_t st);
+
+struct LinearArgs {
+  const uint64_t* in;        // pass input rows
+  const int64_t* in_map;     // optional: physical row of pass-input column (first pass)
+  const uint64_t* round_in;  // round input rows (for extras)
+  const int64_t* round_map;  // physical row of round-input column
+  uint64_t* out;             // output rows
+  const int64_t* out_map;    // optional: physical output row of canonical row
+  const int32_t* groups;     // (G, 6)
+  const int32_t* cols;
+  const int32_t* weights;    // blocks [ncols][16]
+  const int32_t* rows;       // canonical output row per group row
+  const int32_t* ex_ptr;     // optional CSR extras (out_len + 1)
+  const int32_t* ex_col;
+  const int32_t* ex_w;
+  const int64_t* bias;       // optional (out_len,)
+  const uint64_t* unit;      // bias unit payload (lanes - body_off,)
+  int64_t G;
+  int64_t lanes;             // u64 lanes per row (2N for ciphertext rows)
+  int64_t body_off;          // first body lane (N)
+};
+cudaError_t launch_linear(const RingConst& rc, const LinearArgs& a, cudaStream_t st);
+
+}  // namespace sfhr

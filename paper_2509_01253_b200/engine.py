@@ -1,0 +1,321 @@
+"""ServerEngine drop-in: the reference's server round, on one B200.
+
+Keeps the public surface of reference pkg/src/sfhr/protocol.py:145-321 —
+``ServerEngine(model, scheme, master_seed, threads, shuffle_enabled,
+ks_mode, session_timeout, extra_noise_std)``, ``register_client``,
+``open_session``, ``server_round(session_id, round_no, bundles) ->
+(packed, RoundStats)`` — and the protocol errors, so the client / wire /
+session loop around it is unchanged.
+
+Per round, on the device (one stream, no host round trips in between):
+  1. H2D of the uploaded power bundles (k, npow, 2, N)
+  2. partial extraction of all E_in rows            (extract_kernel)
+  3. unshuffle sigma_{r-1} -> W_r -> shuffle sigma_r  (linear passes; the
+     permutations are index maps inside the first/last pass)
+  4. fast packing of all pack groups, level-synchronous (merge + fused
+     key-switch stage kernels)
+  5. D2H of the packed ciphertexts and the live key-switch count.
+sigma_r comes from the C++ port of derive_permutation and is computed for
+the whole session on a host thread when the session opens.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .device import DeviceKey, RingContext, to_dev, to_host_u64
+from .linear import DevicePass, run_round
+from .model import QuantModel, lower_round
+from .params import SchemeParams
+from .tracepack import (extract_device, extraction_payload_for_one, pack_device,
+                        power_exponents, stack_bundles, stage0_chains, stage_reps_above)
+
+# wire error codes (reference wire.py:41-46)
+ERR_STALE_ROUND = 1
+ERR_BAD_SESSION = 2
+ERR_BAD_TYPE = 3
+ERR_MALFORMED = 4
+ERR_PARAM_MISMATCH = 5
+ERR_INTERNAL = 6
+HEADER_SIZE = 35  # reference wire.py:29-32
+
+
+class ProtocolError(Exception):
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+
+def required_ksk_indices(scheme: SchemeParams) -> list:
+    """Automorphism indices the server needs (reference protocol.py:46-59)."""
+    R = scheme.ring
+    idx = set()
+    for j in range(max(scheme.gamma, 1), R.alpha):
+        idx.update(stage_reps_above(j, R)[1:])
+    if scheme.gamma == 0:
+        for ch in stage0_chains(R):
+            idx.update(ch[1:])
+    return sorted(idx)
+
+
+def _block_size(m: int, count: int) -> int:
+    return 4 + 4 + count * 2 * m * 8 + 1
+
+
+def round_req_size(scheme: SchemeParams, k_chunks: int) -> int:
+    """Analytic upload bytes (reference wire.py:265-268)."""
+    npow = len(power_exponents(scheme.gamma, scheme.ring))
+    per = 4 + 4 * npow + _block_size(scheme.ring.M, npow)
+    return HEADER_SIZE + 4 + k_chunks * per
+
+
+def round_resp_size(scheme: SchemeParams, n_packs: int) -> int:
+    return HEADER_SIZE + 4 + _block_size(scheme.ring.M, n_packs)
+
+
+@dataclass
+class RoundMeta:
+    input_len: int
+    output_len: int
+    activation: Optional[str]
+    eta: int
+    clip: tuple
+    skip_source: int
+    skip_len: int
+    final: bool
+
+
+@dataclass
+class ModelMetadata:
+    rounds: list
+    input_shape: tuple
+    input_clip: tuple
+    num_classes: int
+    t: int
+    alpha: int
+    p_bits: int
+    gamma: int
+    beta: int
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "rounds": [vars(r) | {"clip": list(r.clip)} for r in self.rounds],
+            "input_shape": list(self.input_shape), "input_clip": list(self.input_clip),
+            "num_classes": self.num_classes, "t": self.t, "alpha": self.alpha,
+            "p_bits": self.p_bits, "gamma": self.gamma, "beta": self.beta}, sort_keys=True)
+
+
+def metadata_for(model, scheme: SchemeParams) -> ModelMetadata:
+    rounds = [RoundMeta(r.input_len, r.output_len, r.activation, r.eta, tuple(r.clip), r.skip_source,
+                        r.skip_len, r.final) for r in model.rounds]
+    return ModelMetadata(rounds, tuple(model.input_shape), tuple(model.input_clip), model.num_classes,
+                         scheme.ring.t, scheme.ring.alpha, scheme.ring.p_bits, scheme.gamma,
+                         scheme.beta_eff)
+
+
+@dataclass
+class RoundStats:
+    extract_s: float = 0.0
+    linear_s: float = 0.0
+    pack_s: float = 0.0
+    key_switches: int = 0
+    packed_coefficients: int = 0
+    bytes_up: int = 0
+    bytes_down: int = 0
+
+
+@dataclass
+class _SessionState:
+    key_id: bytes
+    next_round: int = 1
+    last_seen: float = field(default_factory=time.monotonic)
+    perms: object = None   # Future -> dict[(round, size)] -> np.ndarray
+
+
+@dataclass
+class _ClientKeys:
+    ksk: object
+    key: DeviceKey
+    scheme: SchemeParams
+
+
+class ServerEngine:
+    """Holds the model and per-client key material; executes server rounds on a B200."""
+
+    def __init__(self, model: QuantModel, scheme: SchemeParams, master_seed: bytes = b"\x00" * 32,
+                 threads: int = 1, shuffle_enabled: bool = True, ks_mode: str = "cuda",
+                 session_timeout: float = 300.0, extra_noise_std: float = 0.0, device: int = 0):
+        if len(master_seed) != 32:
+            raise ValueError("master seed must be 32 bytes")
+        if model.acc_bits != scheme.ring.p_bits:
+            raise ProtocolError(ERR_PARAM_MISMATCH,
+                                "model accumulator width does not match plaintext modulus")
+        if ks_mode not in ("cuda", "fft", "exact"):
+            raise ValueError(f"unknown key-switch mode {ks_mode!r}")
+        self.model = model
+        self.scheme = scheme
+        self.master_seed = master_seed
+        self.threads = max(1, threads)
+        self.shuffle_enabled = shuffle_enabled
+        self.ks_mode = ks_mode
+        self.session_timeout = session_timeout
+        self.extra_noise_std = extra_noise_std
+        self._noise_rng = np.random.default_rng(int.from_bytes(master_seed[:8], "little") ^ 0x6E6F6973)
+        self.ctx = RingContext.for_scheme(scheme, device)
+        self.dev = self.ctx.dev
+        self.clients: dict = {}
+        self.sessions: dict = {}
+        R = scheme.ring
+        unit = extraction_payload_for_one(int(self.ctx.e1[0]), int(self.ctx.e2[0]), scheme.gamma, R,
+                                          self.ctx.inv_m_mod_p)
+        self._bias_unit_host = unit
+        self._bias_unit = to_dev(unit, self.dev)
+        self._passes = [[DevicePass(p, self.dev) for p in lower_round(model, r)]
+                        for r in range(len(model.rounds))]
+        self._perm_pool = ThreadPoolExecutor(max_workers=2)
+        self.total_key_switches = 0
+
+    # -- setup ---------------------------------------------------------------
+
+    def register_client(self, ksk) -> bytes:
+        needed = set(required_ksk_indices(self.scheme))
+        have = set(ksk.indices())
+        if not needed <= have:
+            raise ProtocolError(ERR_PARAM_MISMATCH, f"key-switch keys missing indices {sorted(needed - have)}")
+        key_id = hashlib.blake2b(repr(sorted(have)).encode() + np.asarray(ksk.keys[min(have)][0].a).tobytes(),
+                                 digest_size=16).digest()
+        if key_id not in self.clients:
+            self.clients[key_id] = _ClientKeys(ksk=ksk, key=DeviceKey(self.ctx, ksk), scheme=self.scheme)
+        return key_id
+
+    def _perm_schedule(self, session_id: bytes) -> dict:
+        """All permutations a session will use, keyed by (round_no, size)."""
+        need = set()
+        for r, rnd in enumerate(self.model.rounds, start=1):
+            main = rnd.input_len - rnd.skip_len
+            need.add((r - 1, main))
+            if rnd.skip_len:
+                need.add((rnd.skip_source + 1, rnd.skip_len))
+            if not rnd.final:
+                need.add((r, rnd.output_len))
+        out = {}
+        for (rno, size) in sorted(need):
+            out[(rno, size)] = self._perm_now(session_id, rno, size)
+        return out
+
+    def _perm_now(self, session_id, round_no, size):
+        if not self.shuffle_enabled or round_no == 0:
+            return np.arange(size, dtype=np.int64)
+        return nat.derive_permutation(self.master_seed, session_id, round_no, size)
+
+    def open_session(self, session_id: bytes, key_id: bytes) -> ModelMetadata:
+        if key_id not in self.clients:
+            raise ProtocolError(ERR_BAD_SESSION, "unknown key id")
+        self._reap()
+        if session_id in self.sessions:
+            raise ProtocolError(ERR_BAD_SESSION, "session id already in use")
+        st = _SessionState(key_id=key_id)
+        st.perms = self._perm_pool.submit(self._perm_schedule, session_id)
+        self.sessions[session_id] = st
+        return metadata_for(self.model, self.scheme)
+
+    def _reap(self):
+        now = time.monotonic()
+        for sid in [s for s, st in self.sessions.items() if now - st.last_seen > self.session_timeout]:
+            del self.sessions[sid]
+
+    def _perm(self, state: _SessionState, session_id: bytes, round_no: int, size: int) -> np.ndarray:
+        table = state.perms.result() if state.perms is not None else {}
+        p = table.get((round_no, size))
+        return p if p is not None else self._perm_now(session_id, round_no, size)
+
+    # -- round processing ------------------------------------------------------
+
+    def round_maps(self, state, session_id, round_no):
+        """(in_map, out_map) host int64 arrays for round round_no (protocol.py:243-263)."""
+        rnd = self.model.rounds[round_no - 1]
+        main = rnd.input_len - rnd.skip_len
+        in_map = self._perm(state, session_id, round_no - 1, main)
+        if rnd.skip_len:
+            sk = self._perm(state, session_id, rnd.skip_source + 1, rnd.skip_len) + main
+            in_map = np.concatenate([in_map, sk])
+        out_map = None if rnd.final else self._perm(state, session_id, round_no, rnd.output_len)
+        return in_map, out_map
+
+    def server_round(self, session_id: bytes, round_no: int, bundles: list):
+        state = self.sessions.get(session_id)
+        if state is None:
+            raise ProtocolError(ERR_BAD_SESSION, "unknown or expired session")
+        if round_no != state.next_round:
+            raise ProtocolError(ERR_STALE_ROUND, f"expected round {state.next_round}, got {round_no}")
+        if not (1 <= round_no <= len(self.model.rounds)):
+            raise ProtocolError(ERR_STALE_ROUND, "round beyond model depth")
+        rnd = self.model.rounds[round_no - 1]
+        R = self.scheme.ring
+        keys = self.clients[state.key_id]
+        k_expected = -(-rnd.input_len // R.N)
+        if len(bundles) != k_expected:
+            raise ProtocolError(ERR_MALFORMED, f"expected {k_expected} chunks, got {len(bundles)}")
+        power, exps = stack_bundles(bundles, R)
+        in_map, out_map = self.round_maps(state, session_id, round_no)
+        packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, in_map, out_map)
+        packs_host = to_host_u64(packs_dev)
+        packed = [packs_host[i] for i in range(packs_host.shape[0])]
+        state.next_round += 1
+        state.last_seen = time.monotonic()
+        if round_no == len(self.model.rounds):
+            self.sessions.pop(session_id, None)
+        if self.extra_noise_std > 0:
+            q = float(1 << 53)
+            for pk in packed:
+                extra = np.rint(self._noise_rng.normal(0.0, self.extra_noise_std, pk.shape[-1]) * q)
+                pk[1] = (pk[1] + extra.astype(np.int64).astype(np.uint64)) & np.uint64((1 << 53) - 1)
+        self.total_key_switches += nks
+        st = RoundStats(extract_s=times[0], linear_s=times[1], pack_s=times[2], key_switches=nks,
+                        packed_coefficients=len(packed) * self.scheme.pack_factor,
+                        bytes_up=round_req_size(self.scheme, len(bundles)),
+                        bytes_down=round_resp_size(self.scheme, len(packed)))
+        return packed, st
+
+    def round_device(self, round_no: int, key: DeviceKey, power, exps, in_map, out_map,
+                     timed: bool = True):
+        """Device part of one round. power: host (k, npow, 2, N) uint64 or device tensor.
+
+        Returns (packs_dev, key_switches, (extract_s, linear_s, pack_s)).
+        """
+        rnd = self.model.rounds[round_no - 1]
+        ctx = self.ctx
+        F = self.scheme.pack_factor
+        stream = torch.cuda.current_stream(self.dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timed else None
+        if ev:
+            ev[0].record(stream)
+        pw = power if isinstance(power, torch.Tensor) else to_dev(power, self.dev)
+        rows = extract_device(ctx, pw, exps, rnd.input_len)
+        if ev:
+            ev[1].record(stream)
+        G = -(-rnd.output_len // F)
+        buf = torch.zeros((G * F, 2, ctx.N), dtype=torch.int64, device=self.dev)
+        im = torch.from_numpy(in_map).to(self.dev)
+        om = None if out_map is None else torch.from_numpy(out_map).to(self.dev)
+        run_round(ctx, self._passes[round_no - 1], rows, im, buf, om, self._bias_unit)
+        if ev:
+            ev[2].record(stream)
+        cnt = ctx.counter()
+        packs = pack_device(ctx, key, buf, G, cnt, skip_zero=True)
+        if ev:
+            ev[3].record(stream)
+        nks = int(cnt.item())  # synchronises the stream
+        times = (0.0, 0.0, 0.0)
+        if ev:
+            times = tuple(ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(3))
+        return packs, nks, times

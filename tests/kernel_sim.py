@@ -1,0 +1,208 @@
+"""Bit-level numpy model of the device key-switch stage kernel (test-only).
+
+Replays, with the library's own constant tables (planning-only context, no
+GPU), exactly the arithmetic of ks_stage_kernel / ks_spectra_kernel in
+paper_2509_01253_b200/csrc/keyswitch.cu: Montgomery REDC with lazy [0, 2p)
+ranges, the fused automorphism+decomposition first step, radix-t DIF/DIT
+stages, NTT-domain accumulation over reps, and explicit CRT mod 2^53.
+Every REDC input is range-checked, so an overflow in the kernel's bound
+reasoning fails here on CPU before any GPU time is spent.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from paper_2509_01253_b200 import _native as nat
+
+U = np.uint64
+M32 = U(0xFFFFFFFF)
+
+
+class SimPlan:
+    def __init__(self, t, alpha, p_bits, D, l, gamma=0, beta=0):
+        h = C.c_void_p()
+        nat.check(nat.lib.sfhr_ctx_create(t, alpha, p_bits, D, l, gamma, beta, -1, C.byref(h)))
+        self.h = h
+        rc = nat.RingConst()
+        self.M = t ** alpha
+        npr = rc_np = None  # noqa
+        info = (C.c_int64 * 32)()
+        k = nat.lib.sfhr_ctx_info(h, info, 32)
+        self.info = list(info[:k])
+        np_ = self.info[3]
+        tw = np.zeros(np_ * (self.M + 1), np.uint32)
+        nat.check(nat.lib.sfhr_ctx_debug_tables(h, C.byref(rc), C.sizeof(rc), tw.ctypes.data, tw.size))
+        self.rc = rc
+        self.tw = tw.reshape(np_, self.M + 1).astype(U)
+        self.t, self.alpha, self.N, self.n1 = t, alpha, rc.N, rc.n1
+        self.np, self.l = rc.np, rc.l
+        self.nitems = rc.nitems
+
+    def close(self):
+        nat.lib.sfhr_ctx_destroy(self.h)
+
+
+class Prime:
+    def __init__(self, sp: SimPlan, i: int):
+        pc = sp.rc.pc[i]
+        self.p, self.pinv, self.mu = U(pc.p), U(pc.pinv), U(pc.mu)
+        self.r2, self.rmod = U(pc.r2), U(pc.rmod)
+        T = sp.t
+        self.z = np.array([[pc.z[k][m] for m in range(T)] for k in range(T)], dtype=U)
+        self.zi = np.array([[pc.zi[k][m] for m in range(T)] for k in range(T)], dtype=U)
+        self.g = np.array([[pc.g[j][r] for r in range(T - 1)] for j in range(T - 1)], dtype=U)
+        self.q_mod64 = U(pc.q_mod64)
+        self.inv_p = pc.inv_p
+        self.wt = sp.tw[i]
+
+    def redc(self, x):
+        x = np.asarray(x, dtype=U)
+        hi = x >> U(32)
+        assert np.all(hi < self.p), "REDC input >= p * 2^32"
+        m = ((x & M32) * self.pinv) & M32
+        r = hi + self.p - ((m * self.p) >> U(32))
+        assert np.all((r > 0) & (r < U(2) * self.p))
+        return r
+
+    def redc_wide(self, x):
+        x = np.asarray(x, dtype=U)
+        assert np.all(x < U(1 << 63)), "wide accumulator overflow"
+        hi = x >> U(32)
+        m = ((x & M32) * self.pinv) & M32
+        r = hi + self.p - ((m * self.p) >> U(32))
+        q = (r * self.mu) >> U(32)
+        r = r - q * self.p
+        assert np.all(r < U(2) * self.p)
+        return r
+
+    def mont(self, a, bm):
+        a = np.asarray(a, dtype=U)
+        assert np.all(a < U(2) * self.p)
+        return self.redc(a * np.asarray(bm, dtype=U))
+
+    def dft(self, xs, Z):
+        """xs: list of T arrays; returns T arrays (sum over m of x_m Z[k][m], REDC)."""
+        T = len(xs)
+        out = []
+        for k in range(T):
+            s = np.zeros_like(xs[0], dtype=U)
+            for m in range(T):
+                s = s + xs[m] * Z[k][m]
+            out.append(self.redc(s))
+        return out
+
+
+def forward(sp: SimPlan, pr: Prime, vals):
+    """vals: (N,) residues < 2p (coefficient domain) -> (nitems, T) last-stage outputs."""
+    T, n1, M = sp.t, sp.n1, sp.M
+    A = np.asarray(vals, dtype=U).reshape(T - 1, n1)
+    m = np.arange(n1)
+    buf = np.zeros((T - 1, n1), U)
+    for q in range(1, T):
+        s = np.zeros(n1, U)
+        for j in range(T - 1):
+            s = s + A[j] * pr.z[q][j]
+        buf[q - 1] = pr.mont(pr.redc(s), pr.wt[q * m])
+    buf = buf.reshape(-1)
+    nsub = n1 // T
+    L = nsub
+    for s_ in range(sp.alpha - 2):
+        blocks = T ** s_
+        v = buf.reshape(T - 1, blocks, T, L)
+        step = M // (T * L)
+        j = np.arange(L)
+        xs = [v[:, :, mm, :] for mm in range(T)]
+        ys = pr.dft(xs, pr.z)
+        nv = np.empty_like(v)
+        nv[:, :, 0, :] = ys[0]
+        for k in range(1, T):
+            nv[:, :, k, :] = pr.mont(ys[k], pr.wt[step * j * k][None, None, :])
+        buf = nv.reshape(-1)
+        L //= T
+    x = buf.reshape(sp.nitems, T)
+    ys = pr.dft([x[:, mm] for mm in range(T)], pr.z)
+    return np.stack(ys, axis=1)  # (nitems, T)
+
+
+def inverse(sp: SimPlan, pr: Prime, y):
+    """y: (nitems, T) in [0,2p) -> (N,) CRT-weighted residues y_i in [0, p)."""
+    T, n1, M = sp.t, sp.n1, sp.M
+    xs = pr.dft([y[:, k] for k in range(T)], pr.zi)
+    buf = np.stack(xs, axis=1).reshape(-1)
+    L = T
+    for s_ in range(sp.alpha - 3, -1, -1):
+        blocks = T ** s_
+        v = buf.reshape(T - 1, blocks, T, L)
+        step = M // (T * L)
+        j = np.arange(L)
+        zs = [v[:, :, 0, :]] + [pr.mont(v[:, :, k, :], pr.wt[M - step * j * k][None, None, :])
+                               for k in range(1, T)]
+        xs = pr.dft(zs, pr.zi)
+        buf = np.stack(xs, axis=2).reshape(-1)
+        L *= T
+    v = buf.reshape(T - 1, n1)
+    m = np.arange(n1)
+    Cs = [pr.mont(v[r - 1], pr.wt[M - r * m]) for r in range(1, T)]
+    out = np.zeros((T - 1, n1), U)
+    for j in range(T - 1):
+        s = np.zeros(n1, U)
+        for r in range(T - 1):
+            s = s + Cs[r] * pr.g[j][r]
+        a = pr.redc(s)
+        out[j] = np.where(a >= pr.p, a - pr.p, a)
+    return out.reshape(-1)
+
+
+def key_spectrum(sp: SimPlan, pr: Prime, key_poly):
+    v = np.asarray(key_poly, dtype=U) & U((1 << 53) - 1)
+    c = v.astype(np.int64)
+    c = np.where(v >= U(1 << 52), c - (1 << 53), c)
+    vals = (c % int(pr.p)).astype(U)
+    y = forward(sp, pr, vals)
+    z = pr.mont(y, pr.r2)
+    return np.where(z >= pr.p, z - pr.p, z)  # (nitems, T)
+
+
+def stage_row(sp: SimPlan, x, reps_dinv_keys, identity, decompose, automorph_u64):
+    """Model of stage_body for one row.  reps_dinv_keys: list of (d, keys[l][2] polys)."""
+    N = sp.N
+    Q = (1 << 53) - 1
+    ys = {}
+    for i in range(sp.np):
+        pr = Prime(sp, i)
+        accA = np.zeros((sp.nitems, sp.t), U)
+        accB = np.zeros((sp.nitems, sp.t), U)
+        for d, keys in reps_dinv_keys:
+            y = automorph_u64(x[0], d) if identity else x[0]
+            digs = decompose(y)
+            for li in range(sp.l):
+                dm = np.where(digs[li] < 0, digs[li] + int(pr.p), digs[li]).astype(U)
+                out = forward(sp, pr, dm)
+                accA = accA + out * key_spectrum(sp, pr, keys[li][0])
+                accB = accB + out * key_spectrum(sp, pr, keys[li][1])
+        ya = inverse(sp, pr, pr.redc_wide(accA))
+        yb = inverse(sp, pr, pr.redc_wide(accB))
+        ys[i] = (ya, yb)
+    A = np.zeros(N, U)
+    B = np.zeros(N, U)
+    fa = np.zeros(N)
+    fb = np.zeros(N)
+    for i in range(sp.np):
+        pc = sp.rc.pc[i]
+        A = A + ys[i][0] * U(pc.q_mod64)
+        B = B + ys[i][1] * U(pc.q_mod64)
+        fa = fa + ys[i][0].astype(np.float64) * pc.inv_p
+        fb = fb + ys[i][1].astype(np.float64) * pc.inv_p
+    Pm = U(sp.rc.P_mod64)
+    A = A - np.rint(fa).astype(np.int64).astype(U) * Pm
+    B = B - np.rint(fb).astype(np.int64).astype(U) * Pm
+    bsum = x[1].copy() if identity else np.zeros(N, U)
+    for d, _ in reps_dinv_keys:
+        bsum = bsum + (automorph_u64(x[1], d) if identity else x[1])
+    out = np.empty((2, N), U)
+    out[0] = ((x[0] if identity else U(0)) - A) & U(Q)
+    out[1] = (bsum - B) & U(Q)
+    return out
