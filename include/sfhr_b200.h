@@ -139,6 +139,9 @@ int sfhr_derive_permutation(const uint8_t* master_seed, int seed_len, const uint
 
 const char* sfhr_last_error(void);
 
+/* Number of CUDA kernels this library has launched (process-wide counter). */
+unsigned long long sfhr_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

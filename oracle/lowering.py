@@ -240,7 +240,12 @@ def int_matmul_mod_q(W, rows):
     flat = rows.reshape(rows.shape[0], -1)
     if float(np.abs(W).max(initial=0)) * e_in * (1 << 18) >= 2 ** 53:
         raise OracleModelError("weight magnitude too large for exact lane combination")
-    Wf = W.astype(np.float64)
+    density = np.count_nonzero(W) / max(1, W.size)
+    if density < 0.125 and W.size > 65536:   # reference model.py:395-399
+        from scipy.sparse import csr_matrix
+        Wf = csr_matrix(W.astype(np.float64))
+    else:
+        Wf = W.astype(np.float64)
     acc = np.zeros((e_out, flat.shape[1]), U64)
     for k in range(3):
         limb = ((flat >> U64(18 * k)) & U64((1 << 18) - 1)).astype(np.float64)

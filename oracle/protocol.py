@@ -103,7 +103,7 @@ class OracleServer:
 
     def __init__(self, model, scheme: Scheme, ksk, master_seed=bytes(32),
                  session_id=bytes(16), shuffle=True, ks_mode="exact",
-                 round_mats=None):
+                 round_mats=None, threads=1):
         self.model, self.scheme = model, scheme
         self.rounds = lowering.build_rounds(model.layers)
         self.seed, self.sid, self.shuffle = master_seed, session_id, shuffle
@@ -112,6 +112,9 @@ class OracleServer:
         self.unit = pack.bias_unit(scheme.gamma, scheme.ring)
         self.mats = round_mats if round_mats is not None else \
             [lowering.round_matrix(model.layers, r) for r in self.rounds]
+        # thread pool over chunks / pack groups, as the reference engine (protocol.py:175-178)
+        from concurrent.futures import ThreadPoolExecutor
+        self.pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
 
     def perm(self, r, size):
         if not self.shuffle:
@@ -120,8 +123,21 @@ class OracleServer:
 
     def extract_all(self, bundles, total):
         R = self.scheme.ring
-        parts = [pack.extract(b, min(R.N, total - j * R.N), R) for j, b in enumerate(bundles)]
+        jobs = [(b, min(R.N, total - j * R.N)) for j, b in enumerate(bundles)]
+        one = lambda a: pack.extract(a[0], a[1], R)  # noqa: E731
+        parts = list(self.pool.map(one, jobs)) if self.pool and len(jobs) > 1 else [one(a) for a in jobs]
         return np.concatenate(parts, axis=0)
+
+    def pack_groups(self, out, max_groups=None):
+        """ServerEngine._pack over (a prefix of) the pack groups (protocol.py:296-321)."""
+        groups = pack.pad_groups(out, self.scheme.pack_factor, self.scheme.ring.N)
+        if max_groups is not None:
+            groups = groups[:max_groups]
+        one = lambda g: pack.fast_pack(g, self.scheme, self.engine, counter=self.counter,  # noqa: E731
+                                       skip_zero=True)
+        if self.pool and len(groups) > 1:
+            return list(self.pool.map(one, groups))
+        return [one(g) for g in groups]
 
     def linear_rows(self, round_no, rows):
         """Unshuffle -> W -> shuffle (protocol.py:243-263)."""
@@ -145,7 +161,7 @@ class OracleServer:
         out = self.linear_rows(round_no, rows)
         t2 = time.perf_counter()
         before = self.counter.total_key_switches
-        packs = pack.pack_rows(out, self.scheme, self.engine, counter=self.counter)
+        packs = self.pack_groups(out)
         t3 = time.perf_counter()
         st.extract_s, st.linear_s, st.pack_s = t1 - t0, t2 - t1, t3 - t2
         st.key_switches = self.counter.total_key_switches - before

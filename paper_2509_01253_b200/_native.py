@@ -46,6 +46,7 @@ def _load() -> C.CDLL:
         "sfhr_pack": (i32, [vp, vp, vp, i64, vp, vp, sz, i32, vp, vp]),
         "sfhr_derive_permutation": (i32, [vp, i32, vp, i32, u32, i64, vp]),
         "sfhr_last_error": (C.c_char_p, []),
+        "sfhr_launch_count": (C.c_ulonglong, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -55,6 +56,10 @@ def _load() -> C.CDLL:
 
 
 lib = _load()
+
+
+def launch_count() -> int:
+    return int(lib.sfhr_launch_count())
 
 
 def last_error() -> str:

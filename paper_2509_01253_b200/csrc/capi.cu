@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -40,6 +41,7 @@ struct sfhr_key {
 
 namespace {
 thread_local std::string g_err;
+std::atomic<unsigned long long> g_launches{0};  // kernels launched through this library
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -108,6 +110,7 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     return SFHR_OK;
   }
   CK(launch_stage(P.rc, a, st), "stage kernel");
+  ++g_launches;
   return SFHR_OK;
 }
 }  // namespace
@@ -115,6 +118,8 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
 extern "C" {
 
 const char* sfhr_last_error(void) { return g_err.c_str(); }
+
+unsigned long long sfhr_launch_count(void) { return g_launches.load(); }
 
 int sfhr_ctx_create(int t, int alpha, int p_bits, int D, int l, int gamma, int beta, int device,
                     sfhr_ctx** out) {
@@ -226,6 +231,7 @@ int sfhr_register_ksk(sfhr_ctx* ctx, const uint32_t* idx, int nidx, const uint64
   a.out = key->spectra;
   a.twid = ctx->twid;
   e = launch_spectra(rc, a, nidx * rc.l * 2, (cudaStream_t)stream);
+  if (nidx) ++g_launches;
   if (e != cudaSuccess) {
     cudaFree(key->spectra);
     delete key;
@@ -256,6 +262,7 @@ int sfhr_automorphism_batch(sfhr_ctx* ctx, uint32_t d, const uint64_t* in, uint6
     return fail(SFHR_EINVAL, ex.what());
   }
   CK(launch_automorphism(ctx->plan.rc, dinv, in, out, B, (cudaStream_t)stream), "automorphism kernel");
+  if (B) ++g_launches;
   return SFHR_OK;
 }
 
@@ -304,6 +311,7 @@ int sfhr_extract(sfhr_ctx* ctx, const uint64_t* power, const uint32_t* exps, int
   a.npow = npow;
   a.cu = P.cu;
   CK(launch_extract(P.rc, a, (cudaStream_t)stream), "extract kernel");
+  if (E) ++g_launches;
   return SFHR_OK;
 }
 
@@ -333,6 +341,7 @@ int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* d, void* stream) {
   a.body_off = d->lanes ? d->body_off : ctx->plan.rc.N;
   if (a.lanes > 65535LL * 128) return fail(SFHR_EINVAL, "too many lanes per row");
   CK(launch_linear(ctx->plan.rc, a, (cudaStream_t)stream), "linear kernel");
+  if (a.G) ++g_launches;
   return SFHR_OK;
 }
 
@@ -371,6 +380,7 @@ int sfhr_pack(sfhr_ctx* ctx, const sfhr_key* key, uint64_t* rows, int64_t G, uin
       const int members = j == 1 ? t - 1 : t;
       const int rest = (int)(per / members);
       CK(launch_merge(rc, cur, oth, G, members, rest, (int)(rc.M / tj), st), "merge kernel");
+      ++g_launches;
       std::swap(cur, oth);
       per = rest;
       if (j <= beta - 1 && j >= std::max(gamma, 1))

@@ -267,7 +267,9 @@ class ServerEngine:
             raise ProtocolError(ERR_MALFORMED, f"expected {k_expected} chunks, got {len(bundles)}")
         power, exps = stack_bundles(bundles, R)
         in_map, out_map = self.round_maps(state, session_id, round_no)
-        packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, in_map, out_map)
+        im = torch.from_numpy(in_map).to(self.dev, non_blocking=True)
+        om = None if out_map is None else torch.from_numpy(out_map).to(self.dev, non_blocking=True)
+        packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, im, om)
         packs_host = to_host_u64(packs_dev)
         packed = [packs_host[i] for i in range(packs_host.shape[0])]
         state.next_round += 1
@@ -288,7 +290,8 @@ class ServerEngine:
 
     def round_device(self, round_no: int, key: DeviceKey, power, exps, in_map, out_map,
                      timed: bool = True):
-        """Device part of one round. power: host (k, npow, 2, N) uint64 or device tensor.
+        """Device part of one round. power: host (k, npow, 2, N) uint64 or device tensor;
+        in_map / out_map: device int64 tensors (out_map None for the final round).
 
         Returns (packs_dev, key_switches, (extract_s, linear_s, pack_s)).
         """
@@ -305,9 +308,7 @@ class ServerEngine:
             ev[1].record(stream)
         G = -(-rnd.output_len // F)
         buf = torch.zeros((G * F, 2, ctx.N), dtype=torch.int64, device=self.dev)
-        im = torch.from_numpy(in_map).to(self.dev)
-        om = None if out_map is None else torch.from_numpy(out_map).to(self.dev)
-        run_round(ctx, self._passes[round_no - 1], rows, im, buf, om, self._bias_unit)
+        run_round(ctx, self._passes[round_no - 1], rows, in_map, buf, out_map, self._bias_unit)
         if ev:
             ev[2].record(stream)
         cnt = ctx.counter()
