@@ -142,6 +142,12 @@ const char* sfhr_last_error(void);
 /* Number of CUDA kernels this library has launched (process-wide counter). */
 unsigned long long sfhr_launch_count(void);
 
+/* Live kernel timing: when enabled, every key-switch stage launch is
+ * bracketed by CUDA events on its stream; collect() waits for them and
+ * returns the summed device time, algorithmic bytes (rows * 32 N) and count. */
+int sfhr_profile_enable(sfhr_ctx* ctx, int enable);
+int sfhr_profile_collect(sfhr_ctx* ctx, double* total_ms, long long* total_bytes, long long* launches);
+
 #ifdef __cplusplus
 }
 #endif

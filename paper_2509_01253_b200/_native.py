@@ -47,6 +47,9 @@ def _load() -> C.CDLL:
         "sfhr_derive_permutation": (i32, [vp, i32, vp, i32, u32, i64, vp]),
         "sfhr_last_error": (C.c_char_p, []),
         "sfhr_launch_count": (C.c_ulonglong, []),
+        "sfhr_profile_enable": (i32, [vp, i32]),
+        "sfhr_profile_collect": (i32, [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong),
+                                       C.POINTER(C.c_longlong)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -60,6 +63,12 @@ lib = _load()
 
 def launch_count() -> int:
     return int(lib.sfhr_launch_count())
+
+
+def profile_collect(ctx_handle) -> tuple[float, int, int]:
+    ms, by, n = C.c_double(), C.c_longlong(), C.c_longlong()
+    check(lib.sfhr_profile_collect(ctx_handle, C.byref(ms), C.byref(by), C.byref(n)))
+    return ms.value, by.value, n.value
 
 
 def last_error() -> str:

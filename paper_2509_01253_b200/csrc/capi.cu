@@ -24,9 +24,17 @@ void derive_permutation(const uint8_t* seed, int seed_len, const uint8_t* sid, i
 
 using namespace sfhr;
 
+struct ProfRec {
+  cudaEvent_t a, b;
+  long long bytes;
+};
+
 struct sfhr_ctx {
   Plan plan;
   int device = 0;
+  bool prof = false;                 // time every stage launch with CUDA events
+  std::vector<ProfRec> prof_recs;    // pending (unresolved) records
+  std::vector<cudaEvent_t> ev_pool;  // recycled events
   uint32_t* twid = nullptr;  // [np][M+1]
   int32_t* cvec = nullptr;   // [N]
   std::mutex mu;
@@ -105,12 +113,28 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     ++ns;
   }
   a.nreps = ns;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (ctx->prof && ns > 0 && B > 0) {
+    for (cudaEvent_t* e : {&e0, &e1}) {
+      if (!ctx->ev_pool.empty()) {
+        *e = ctx->ev_pool.back();
+        ctx->ev_pool.pop_back();
+      } else {
+        CK(cudaEventCreate(e), "event create");
+      }
+    }
+    CK(cudaEventRecord(e0, st), "event record");
+  }
   if (ns == 0) {
     if (in != out) CK(cudaMemcpyAsync(out, in, (size_t)B * 2 * P.rc.N * 8, cudaMemcpyDeviceToDevice, st), "stage copy");
     return SFHR_OK;
   }
   CK(launch_stage(P.rc, a, st), "stage kernel");
   ++g_launches;
+  if (e0) {
+    CK(cudaEventRecord(e1, st), "event record");
+    ctx->prof_recs.push_back({e0, e1, (long long)B * 32LL * P.rc.N});
+  }
   return SFHR_OK;
 }
 }  // namespace
@@ -120,6 +144,36 @@ extern "C" {
 const char* sfhr_last_error(void) { return g_err.c_str(); }
 
 unsigned long long sfhr_launch_count(void) { return g_launches.load(); }
+
+int sfhr_profile_enable(sfhr_ctx* ctx, int enable) {
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->prof = enable != 0;
+  return SFHR_OK;
+}
+
+int sfhr_profile_collect(sfhr_ctx* ctx, double* total_ms, long long* total_bytes, long long* launches) {
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g(ctx->device);
+  double ms = 0;
+  long long by = 0, n = 0;
+  for (auto& r : ctx->prof_recs) {
+    CK(cudaEventSynchronize(r.b), "event sync");
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, r.a, r.b), "event elapsed");
+    ms += t;
+    by += r.bytes;
+    ++n;
+    ctx->ev_pool.push_back(r.a);
+    ctx->ev_pool.push_back(r.b);
+  }
+  ctx->prof_recs.clear();
+  if (total_ms) *total_ms = ms;
+  if (total_bytes) *total_bytes = by;
+  if (launches) *launches = n;
+  return SFHR_OK;
+}
 
 int sfhr_ctx_create(int t, int alpha, int p_bits, int D, int l, int gamma, int beta, int device,
                     sfhr_ctx** out) {
@@ -160,6 +214,11 @@ int sfhr_ctx_destroy(sfhr_ctx* ctx) {
     return SFHR_OK;
   }
   DeviceGuard g(ctx->device);
+  for (auto& r : ctx->prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaFree(ctx->twid);
   cudaFree(ctx->cvec);
   delete ctx;

@@ -240,6 +240,26 @@ class ServerEngine:
 
     # -- round processing ------------------------------------------------------
 
+    def _upload_bundles(self, bundles):
+        """Stage the uploads in pinned host memory and copy them to the device."""
+        R = self.scheme.ring
+        exps = sorted(bundles[0].power_cts)
+        shape = (len(bundles), len(exps), 2, R.N)
+        n = int(np.prod(shape))
+        if getattr(self, "_pinned", None) is None or self._pinned.numel() < n:
+            self._pinned = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        host = self._pinned[:n].numpy().view(np.uint64).reshape(shape)
+        for j, b in enumerate(bundles):
+            if set(b.power_cts) != set(exps) or set(exps) != set(power_exponents(b.gamma, R)):
+                raise ValueError(f"bundle exponents {sorted(b.power_cts)} != required "
+                                 f"{sorted(power_exponents(self.scheme.gamma, R))}")
+            for q, d in enumerate(exps):
+                ct = b.power_cts[d]
+                host[j, q, 0] = ct.a
+                host[j, q, 1] = ct.b
+        dev = self._pinned[:n].view(shape).to(self.dev, non_blocking=True)
+        return dev, exps
+
     def round_maps(self, state, session_id, round_no):
         """(in_map, out_map) host int64 arrays for round round_no (protocol.py:243-263)."""
         rnd = self.model.rounds[round_no - 1]
@@ -265,7 +285,7 @@ class ServerEngine:
         k_expected = -(-rnd.input_len // R.N)
         if len(bundles) != k_expected:
             raise ProtocolError(ERR_MALFORMED, f"expected {k_expected} chunks, got {len(bundles)}")
-        power, exps = stack_bundles(bundles, R)
+        power, exps = self._upload_bundles(bundles)
         in_map, out_map = self.round_maps(state, session_id, round_no)
         im = torch.from_numpy(in_map).to(self.dev, non_blocking=True)
         om = None if out_map is None else torch.from_numpy(out_map).to(self.dev, non_blocking=True)

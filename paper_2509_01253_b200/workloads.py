@@ -19,6 +19,10 @@ from .model import LayerSpec, QuantModel
 
 
 def _quantize(w: np.ndarray, bits: int) -> np.ndarray:
+    """Symmetric per-tensor quantization; 2-bit uses the ternary threshold 0.7 * mean|w|."""
+    if bits == 2:
+        thr = 0.7 * np.abs(w).mean()
+        return (np.sign(w) * (np.abs(w) > thr)).astype(np.int64)
     qmax = (1 << (bits - 1)) - 1
     s = np.abs(w).max() / qmax if np.abs(w).max() > 0 else 1.0
     return np.clip(np.rint(w / s), -qmax, qmax).astype(np.int64)
