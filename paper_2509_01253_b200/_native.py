@@ -111,7 +111,7 @@ class RingConst(C.Structure):
     _fields_ = [(n, C.c_int) for n in ("t", "alpha", "M", "N", "n1", "nitems", "np", "l", "D",
                                        "dlog2", "shift")] + \
                [("magicM", C.c_uint32), ("magicN1", C.c_uint32), ("P_mod64", C.c_uint64),
-                ("pc", PrimeConst * 4)]
+                ("decM", C.c_uint64 * 5), ("decDp", C.c_uint64 * 5), ("pc", PrimeConst * 4)]
 
 
 assert C.sizeof(RingConst) == lib.sfhr_ringconst_bytes(), "RingConst layout mismatch"

@@ -50,39 +50,31 @@ __device__ __forceinline__ void dft_t(const uint32_t (&x)[T], uint32_t (&y)[T],
   }
 }
 
-// balanced base-D decomposition of y < 2^53 into L signed digits
-template <int L>
-__device__ __forceinline__ void decompose(uint64_t y, int (&dg)[L], const RingConst& rc) {
+// Digit i (0 = most significant) of the balanced base-D decomposition of
+// y < 2^53, in closed form so a digit can be produced without the others
+// (reference crypto.py:288-323 computes them as a carry chain):
+//  * D = 2^w:  u = round(y D^l / q); digit i = raw_i + c_i centred, where
+//    raw_i = (u >> w(l-1-i)) & (D-1) and the carry c_i = [u mod D^(l-1-i) > M_i]
+//    with M_i the largest balanced value of the lower digits;
+//  * odd D:   with F_i = round_half_up(r D^(i+1) / q), r the centred y,
+//    digit i = F_i - D F_(i-1)   (telescoping the reference's iteration).
+__device__ __forceinline__ int digit_i(uint64_t y, int i, const RingConst& rc) {
   if (rc.dlog2 >= 0) {
     const int w = rc.dlog2;
-    const int D = rc.D;
-    uint64_t u = (y + (1ull << (rc.shift - 1))) >> rc.shift;
-    int raw[L];
-#pragma unroll
-    for (int i = L - 1; i >= 0; --i) {
-      raw[i] = (int)(u & (uint64_t)(D - 1));
-      u >>= w;
-    }
-    int carry = 0;
-#pragma unroll
-    for (int i = L - 1; i >= 0; --i) {
-      int x = raw[i] + carry;
-      int over = x > (D >> 1);
-      dg[i] = over ? x - D : x;
-      carry = over;
-    }
-  } else {
-    const long long D = rc.D;
-    long long r = (long long)y;
-    if (y > (1ull << 52)) r -= (1ll << 53);
-#pragma unroll
-    for (int i = 0; i < L; ++i) {
-      long long prod = r * D;
-      long long d = (prod + (1ll << 52)) >> 53;
-      dg[i] = (int)d;
-      r = prod - d * (1ll << 53);
-    }
+    const uint64_t u = (y + (1ull << (rc.shift - 1))) >> rc.shift;
+    const int low = w * (rc.l - 1 - i);
+    const int raw = (int)((u >> low) & (uint64_t)(rc.D - 1));
+    const uint64_t lower = u & ((1ull << low) - 1ull);
+    const int x = raw + (lower > rc.decM[i] ? 1 : 0);
+    return x > (rc.D >> 1) ? x - rc.D : x;
   }
+  long long r = (long long)y;
+  if (y > (1ull << 52)) r -= (1ll << 53);
+  const __int128 half = (__int128)1 << 52;
+  const long long Fi = (long long)(((__int128)r * (__int128)rc.decDp[i] + half) >> 53);
+  if (i == 0) return (int)Fi;
+  const long long Fp = (long long)(((__int128)r * (__int128)rc.decDp[i - 1] + half) >> 53);
+  return (int)(Fi - (long long)rc.D * Fp);
 }
 
 __device__ __forceinline__ uint32_t lift_signed(int d, uint32_t p) {
@@ -175,17 +167,18 @@ __device__ void inv_first_step(uint32_t* buf, int nb, const RingConst& rc, const
 // the fused stage kernel
 
 struct SmemLayout {
-  uint64_t* xa;
-  uint32_t* wt;
-  uint32_t* buf;
+  uint64_t* xa;   // (N,) staged mask component of the row
+  uint32_t* wt;   // (M+1,) Montgomery twiddles of this CTA's prime
+  uint32_t* acc;  // (2, N) NTT-domain accumulators, summed over reps
+  uint32_t* buf;  // (nb, N) transform buffers
 };
 
-__device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst& rc, int nbuf) {
+__device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst& rc) {
   SmemLayout s;
   s.xa = reinterpret_cast<uint64_t*>(smem);
   s.wt = reinterpret_cast<uint32_t*>(smem + (size_t)rc.N * 8);
-  s.buf = s.wt + ((rc.M + 1 + 3) & ~3);
-  (void)nbuf;
+  s.acc = s.wt + ((rc.M + 1 + 3) & ~3);
+  s.buf = s.acc + 2 * rc.N;
   return s;
 }
 
@@ -194,8 +187,7 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   const PrimeConst& pc = rc.pc[PR];
   const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
   const int N = rc.N, n1 = rc.n1, M = rc.M;
-  const int nb = L > 2 ? L : 2;
-  SmemLayout S = carve(smem, rc, nb);
+  SmemLayout S = carve(smem, rc);
   const int64_t row = blockIdx.x / rc.np;
   const uint64_t* xin = a.in + row * 2 * (int64_t)N;
   uint64_t* xout = a.out + row * 2 * (int64_t)N;
@@ -226,34 +218,28 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
 
   const int item = threadIdx.x;
   const bool owner = item < rc.nitems;
-  uint64_t accA[T], accB[T];
-#pragma unroll
-  for (int k = 0; k < T; ++k) accA[k] = accB[k] = 0;
 
   for (int r = 0; r < a.nreps; ++r) {
     const uint32_t dinv = a.dinv[r];
     const uint32_t step1 = fastmod((uint32_t)n1 * dinv, M, rc.magicM);
-    // ---- forward first step with fused automorphism + decomposition ----
+    // ---- forward first step with fused automorphism + per-digit decomposition ----
     for (int m = threadIdx.x; m < n1; m += blockDim.x) {
-      uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
+      const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
       const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
       uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
-      int dg[L][T - 1];
+      uint64_t y[T - 1];
 #pragma unroll
       for (int j = 0; j < T - 1; ++j) {
         const uint64_t v1 = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
-        int d[L];
-        decompose<L>((v1 - v2) & QMASK, d, rc);
-#pragma unroll
-        for (int i = 0; i < L; ++i) dg[i][j] = d[i];
+        y[j] = (v1 - v2) & QMASK;
         s1 += step1;
         if (s1 >= (uint32_t)M) s1 -= M;
       }
-#pragma unroll
+#pragma unroll 1
       for (int i = 0; i < L; ++i) {
         uint32_t vals[T - 1];
 #pragma unroll
-        for (int j = 0; j < T - 1; ++j) vals[j] = lift_signed(dg[i][j], p);
+        for (int j = 0; j < T - 1; ++j) vals[j] = lift_signed(digit_i(y[j], i, rc), p);
         uint32_t* o = S.buf + i * N + m;
 #pragma unroll
         for (int q = 1; q < T; ++q) {
@@ -269,30 +255,32 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
     // ---- last stage (span 1) in registers, MAC against the key spectra ----
     if (owner) {
       const uint32_t* ks = a.spec[r];
+      uint64_t ta[T], tb[T];
 #pragma unroll
+      for (int k = 0; k < T; ++k) ta[k] = tb[k] = 0;
+#pragma unroll 1
       for (int i = 0; i < L; ++i) {
         const uint32_t* v = S.buf + i * N + item * T;
-        uint32_t x[T], y[T];
+        uint32_t x[T], yv[T];
 #pragma unroll
         for (int m = 0; m < T; ++m) x[m] = v[m];
-        dft_t<T>(x, y, pc.z, p, pinv);
+        dft_t<T>(x, yv, pc.z, p, pinv);
         const uint32_t* ka = ks + ((size_t)(i * 2 + 0) * rc.np + PR) * N + item;
         const uint32_t* kb = ks + ((size_t)(i * 2 + 1) * rc.np + PR) * N + item;
 #pragma unroll
         for (int k = 0; k < T; ++k) {
-          accA[k] += (uint64_t)y[k] * __ldg(ka + k * rc.nitems);
-          accB[k] += (uint64_t)y[k] * __ldg(kb + k * rc.nitems);
+          ta[k] += (uint64_t)yv[k] * __ldg(ka + k * rc.nitems);
+          tb[k] += (uint64_t)yv[k] * __ldg(kb + k * rc.nitems);
         }
       }
-      if (a.shrink) {
+      // L products of (<2p)(<p) < p 2^32 (p < 2^31/L): one REDC each; sum over reps < 2 reps p
+      uint32_t* aa = S.acc + item * T;
+      uint32_t* ab = S.acc + N + item * T;
 #pragma unroll
-        for (int k = 0; k < T; ++k) {
-          uint32_t ha = (uint32_t)(accA[k] >> 32), hb = (uint32_t)(accB[k] >> 32);
-          ha -= __umulhi(ha, mu) * p;
-          hb -= __umulhi(hb, mu) * p;
-          accA[k] = (uint64_t)ha * pc.rmod + (uint32_t)accA[k];
-          accB[k] = (uint64_t)hb * pc.rmod + (uint32_t)accB[k];
-        }
+      for (int k = 0; k < T; ++k) {
+        const uint32_t ra = redc(ta[k], p, pinv), rb = redc(tb[k], p, pinv);
+        aa[k] = r ? aa[k] + ra : ra;
+        ab[k] = r ? ab[k] + rb : rb;
       }
     }
     __syncthreads();
@@ -303,8 +291,9 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
     uint32_t za[T], zb[T], xa[T], xb[T];
 #pragma unroll
     for (int k = 0; k < T; ++k) {
-      za[k] = redc_wide(accA[k], p, pinv, mu);
-      zb[k] = redc_wide(accB[k], p, pinv, mu);
+      const uint32_t va = S.acc[item * T + k], vb = S.acc[N + item * T + k];
+      za[k] = va - __umulhi(va, mu) * p;  // -> [0, 2p)
+      zb[k] = vb - __umulhi(vb, mu) * p;
     }
     dft_t<T>(za, xa, pc.zi, p, pinv);
     dft_t<T>(zb, xb, pc.zi, p, pinv);
@@ -355,9 +344,15 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   cluster.sync();
 }
 
+template <int T>
+struct StageLaunch {
+  static constexpr int kThreads = T == 7 ? 320 : 512;
+  static constexpr int kMinBlocks = T == 7 ? 3 : 2;
+};
+
 template <int T, int L>
-__global__ void __launch_bounds__(512) ks_stage_kernel(const __grid_constant__ RingConst rc,
-                                                       const __grid_constant__ StageArgs a) {
+__global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMinBlocks)
+    ks_stage_kernel(const __grid_constant__ RingConst rc, const __grid_constant__ StageArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const unsigned rank = cg::this_cluster().block_rank();
   switch (rank) {
@@ -377,7 +372,7 @@ template <int T, int PR>
 __device__ void spectra_body(const RingConst& rc, const SpecArgs a, unsigned char* smem, int job) {
   const PrimeConst& pc = rc.pc[PR];
   const int N = rc.N, n1 = rc.n1;
-  SmemLayout S = carve(smem, rc, 1);
+  SmemLayout S = carve(smem, rc);
   const uint64_t* src = a.keys + (size_t)job * N;  // job = (slot*l + i)*2 + c
   for (int k = threadIdx.x; k <= rc.M; k += blockDim.x) S.wt[k] = a.twid[(size_t)PR * (rc.M + 1) + k];
   __syncthreads();
@@ -432,7 +427,7 @@ __global__ void __launch_bounds__(512) ks_spectra_kernel(const __grid_constant__
 
 size_t stage_smem_bytes(const RingConst& rc) {
   const int nb = rc.l > 2 ? rc.l : 2;
-  return (size_t)rc.N * 8 + (size_t)((rc.M + 1 + 3) & ~3) * 4 + (size_t)nb * rc.N * 4;
+  return (size_t)rc.N * 8 + (size_t)((rc.M + 1 + 3) & ~3) * 4 + (size_t)(2 + nb) * rc.N * 4;
 }
 
 int stage_threads(const RingConst& rc) { return ((rc.nitems + 31) / 32) * 32; }
@@ -442,6 +437,8 @@ static cudaError_t launch_stage_tl(const RingConst& rc, const StageArgs& a, cuda
   auto kern = ks_stage_kernel<T, L>;
   const size_t smem = stage_smem_bytes(rc);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.B * rc.np), 1, 1);

@@ -130,7 +130,23 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
     rc.dlog2 = -1;
     rc.shift = 0;
   }
-  if (rc.nitems > 1024) throw std::invalid_argument("ring too large for one CTA per row (N/t > 1024)");
+  {
+    const int cap = t == 7 ? 320 : 512;  // StageLaunch<T>::kThreads (keyswitch.cu)
+    if (((rc.nitems + 31) / 32) * 32 > cap)
+      throw std::invalid_argument("ring too large for one CTA per row on this device path");
+  }
+  // per-digit closed forms of the balanced decomposition (see keyswitch.cu digit_i)
+  for (int i = 0; i < l; ++i) {
+    unsigned __int128 Mi = 0, pw = 1;
+    for (int k = l - 1; k > i; --k) {
+      Mi += (unsigned __int128)(D / 2) * pw;
+      pw *= (unsigned __int128)D;
+    }
+    rc.decM[i] = (uint64_t)Mi;
+    unsigned __int128 dp = 1;
+    for (int k = 0; k <= i; ++k) dp *= (unsigned __int128)D;
+    rc.decDp[i] = (uint64_t)dp;
+  }
   rc.magicM = (uint32_t)((1ull << 32) / (uint64_t)rc.M);
   rc.magicN1 = (uint32_t)((1ull << 32) / (uint64_t)rc.n1);
 
@@ -182,12 +198,10 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
   rc.np = (int)primes.size();
   P.bound_bits = (double)bound_bits;
   P.crt_bits = (double)pbits;
-  // accumulator headroom: maxreps * l products of (< 2p) * (< p) must stay < 2^63
-  {
-    long double pm = (long double)primes[0];
-    long double tot = (long double)maxreps * l * 2.0L * pm * pm;
-    P.shrink = tot >= 9.2e18L ? 1 : 0;
-  }
+  // accumulator headroom: each rep adds one REDC output (< 2p) to a u32
+  if (2.0L * maxreps * (long double)primes[0] >= 4294967296.0L)
+    throw std::invalid_argument("NTT-domain accumulator would overflow 32 bits");
+  P.shrink = 0;
 
   uint64_t Pmod = 1;
   for (uint64_t p : primes) Pmod *= p;

@@ -41,6 +41,8 @@ struct RingConst {
   uint32_t magicM;                   // floor(2^32 / M)
   uint32_t magicN1;                  // floor(2^32 / n1)
   uint64_t P_mod64;                  // prod p_i mod 2^64
+  uint64_t decM[MAXL];               // pow2 gadget: carry threshold of digit i (balanced lower part max)
+  uint64_t decDp[MAXL];              // odd gadget: D^(i+1)
   PrimeConst pc[MAXNP];
 };
 

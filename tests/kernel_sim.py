@@ -178,13 +178,21 @@ def stage_row(sp: SimPlan, x, reps_dinv_keys, identity, decompose, automorph_u64
         for d, keys in reps_dinv_keys:
             y = automorph_u64(x[0], d) if identity else x[0]
             digs = decompose(y)
+            ta = np.zeros((sp.nitems, sp.t), U)
+            tb = np.zeros((sp.nitems, sp.t), U)
             for li in range(sp.l):
                 dm = np.where(digs[li] < 0, digs[li] + int(pr.p), digs[li]).astype(U)
                 out = forward(sp, pr, dm)
-                accA = accA + out * key_spectrum(sp, pr, keys[li][0])
-                accB = accB + out * key_spectrum(sp, pr, keys[li][1])
-        ya = inverse(sp, pr, pr.redc_wide(accA))
-        yb = inverse(sp, pr, pr.redc_wide(accB))
+                ta = ta + out * key_spectrum(sp, pr, keys[li][0])
+                tb = tb + out * key_spectrum(sp, pr, keys[li][1])
+            accA = accA + pr.redc(ta)   # one REDC per rep into a u32 accumulator
+            accB = accB + pr.redc(tb)
+            assert np.all(accA < U(1 << 32)) and np.all(accB < U(1 << 32))
+        barrett = lambda v: v - ((v * pr.mu) >> U(32)) * pr.p  # noqa: E731
+        za, zb = barrett(accA), barrett(accB)
+        assert np.all(za < U(2) * pr.p) and np.all(zb < U(2) * pr.p)
+        ya = inverse(sp, pr, za)
+        yb = inverse(sp, pr, zb)
         ys[i] = (ya, yb)
     A = np.zeros(N, U)
     B = np.zeros(N, U)

@@ -126,3 +126,34 @@ def test_stage_kernel_arithmetic_simulation(t, alpha, b, gamma, D, l):
         assert np.array_equal(got, want)
     finally:
         sp.close()
+
+
+@pytest.mark.parametrize("b,gamma", [(8, 0), (12, 0), (12, 1), (16, 0), (16, 1)])
+def test_closed_form_digits_match_reference_decomposition(b, gamma):
+    """The device's per-digit closed forms (keyswitch.cu digit_i) with the library's
+    decM / decDp tables reproduce reference crypto.gadget_decompose exactly."""
+    import kernel_sim as ks
+    sch = osc.preset(b, gamma)
+    R, g = sch.ring, sch.gadget
+    sp = ks.SimPlan(R.t, R.alpha, R.p_bits, g.D, g.l, gamma)
+    try:
+        rc = sp.rc
+        v = u53(9, 3000)
+        v[:6] = [0, 1, (1 << 53) - 1, 1 << 52, (1 << 52) + 1, (1 << 53) // g.D]
+        want = oks.decompose(v, g)
+
+        def digit(y, i):
+            y = int(y)
+            if rc.dlog2 >= 0:
+                u = (y + (1 << (rc.shift - 1))) >> rc.shift
+                low = rc.dlog2 * (rc.l - 1 - i)
+                x = ((u >> low) & (rc.D - 1)) + (1 if (u & ((1 << low) - 1)) > rc.decM[i] else 0)
+                return x - rc.D if x > rc.D // 2 else x
+            r = y - (1 << 53) if y > (1 << 52) else y
+            F = lambda k: (r * rc.decDp[k] + (1 << 52)) >> 53  # noqa: E731
+            return F(i) - (rc.D * F(i - 1) if i else 0)
+
+        got = np.array([[digit(y, i) for y in v] for i in range(g.l)])
+        assert np.array_equal(got, want)
+    finally:
+        sp.close()
