@@ -15,16 +15,19 @@
 // switch_batch (one rep, d_r = 1, no identity term) otherwise.
 //
 // Device design: one thread-block CLUSTER per row, one CTA per CRT prime.
-// Each CTA stages x.a in shared memory, and for every rep computes the
-// automorphism gather + digit decomposition on the fly inside the first
-// transform step, runs the l digit Phi_M-NTTs together (one barrier per
-// radix-t stage), and multiply-accumulates the last butterfly outputs into
-// per-thread 64-bit register accumulators against the precomputed key
-// spectra (thread-owned layout => coalesced).  The reps are summed in the
-// NTT domain, so only 2 inverse transforms per prime per row are needed.
-// Finally the CTAs of the cluster exchange their residues through
-// distributed shared memory and each reconstructs a 1/NP slice of the row by
-// explicit CRT mod 2^53.
+// Per rep, a CTA
+//   A. gathers aut_{d_r}(x.a) from the row staged in shared memory and
+//      decomposes every coefficient into its l balanced digits (balanced over
+//      all N coefficients), lifted mod p into the l transform buffers;
+//   B. runs the first Phi_M-NTT step in place, then the radix-t DIF stages of
+//      all l digit transforms together (one barrier per stage);
+//   C. computes the last (span-1) butterflies in registers and multiply-
+//      accumulates them against the precomputed key spectra (thread-owned
+//      layout => coalesced) into NTT-domain accumulators in shared memory.
+// Reps are summed in the NTT domain, so a row needs only 2 inverse
+// transforms per prime.  The CTAs of the cluster then exchange residues
+// through distributed shared memory and each reconstructs a 1/NP slice of
+// the row by explicit CRT mod 2^53.
 #include <cooperative_groups.h>
 
 #include "sfhr_common.cuh"
@@ -35,8 +38,24 @@ namespace cg = cooperative_groups;
 namespace sfhr {
 
 // ---------------------------------------------------------------------------
-// small DFT helpers (constants come from the __grid_constant__ parameter
-// block with compile-time offsets -> constant-bank operands)
+// geometry: compile-time when the tower height A is a template argument
+
+constexpr int cpow(int b, int e) { return e <= 0 ? 1 : b * cpow(b, e - 1); }
+
+template <int T, int A>
+struct Geo {
+  const int alpha, M, n1, N, nitems;
+  __device__ __forceinline__ explicit Geo(const RingConst& rc)
+      : alpha(A ? A : rc.alpha),
+        M(A ? cpow(T, A) : rc.M),
+        n1(A ? cpow(T, A - 1) : rc.n1),
+        N(A ? cpow(T, A - 1) * (T - 1) : rc.N),
+        nitems(A ? cpow(T, A - 1) * (T - 1) / T : rc.nitems) {}
+};
+
+// ---------------------------------------------------------------------------
+// small DFT helper (constants come from the __grid_constant__ parameter block
+// at compile-time offsets -> uniform-register operands of IMAD.WIDE.U32)
 
 template <int T>
 __device__ __forceinline__ void dft_t(const uint32_t (&x)[T], uint32_t (&y)[T],
@@ -50,31 +69,32 @@ __device__ __forceinline__ void dft_t(const uint32_t (&x)[T], uint32_t (&y)[T],
   }
 }
 
-// Digit i (0 = most significant) of the balanced base-D decomposition of
-// y < 2^53, in closed form so a digit can be produced without the others
-// (reference crypto.py:288-323 computes them as a carry chain):
-//  * D = 2^w:  u = round(y D^l / q); digit i = raw_i + c_i centred, where
-//    raw_i = (u >> w(l-1-i)) & (D-1) and the carry c_i = [u mod D^(l-1-i) > M_i]
-//    with M_i the largest balanced value of the lower digits;
-//  * odd D:   with F_i = round_half_up(r D^(i+1) / q), r the centred y,
-//    digit i = F_i - D F_(i-1)   (telescoping the reference's iteration).
-__device__ __forceinline__ int digit_i(uint64_t y, int i, const RingConst& rc) {
+// balanced base-D digits of y < 2^53 (reference crypto.py:288-323), all at once
+template <int L>
+__device__ __forceinline__ void decompose(uint64_t y, int (&dg)[L], const RingConst& rc) {
   if (rc.dlog2 >= 0) {
-    const int w = rc.dlog2;
-    const uint64_t u = (y + (1ull << (rc.shift - 1))) >> rc.shift;
-    const int low = w * (rc.l - 1 - i);
-    const int raw = (int)((u >> low) & (uint64_t)(rc.D - 1));
-    const uint64_t lower = u & ((1ull << low) - 1ull);
-    const int x = raw + (lower > rc.decM[i] ? 1 : 0);
-    return x > (rc.D >> 1) ? x - rc.D : x;
+    const int w = rc.dlog2, D = rc.D;
+    uint64_t u = (y + (1ull << (rc.shift - 1))) >> rc.shift;
+    int carry = 0;
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) {
+      const int x = (int)(u & (uint64_t)(D - 1)) + carry;
+      u >>= w;
+      carry = x > (D >> 1);
+      dg[i] = carry ? x - D : x;
+    }
+  } else {
+    const long long D = rc.D;
+    long long r = (long long)y;
+    if (y > (1ull << 52)) r -= (1ll << 53);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const long long prod = r * D;
+      const long long d = (prod + (1ll << 52)) >> 53;
+      dg[i] = (int)d;
+      r = prod - d * (1ll << 53);
+    }
   }
-  long long r = (long long)y;
-  if (y > (1ull << 52)) r -= (1ll << 53);
-  const __int128 half = (__int128)1 << 52;
-  const long long Fi = (long long)(((__int128)r * (__int128)rc.decDp[i] + half) >> 53);
-  if (i == 0) return (int)Fi;
-  const long long Fp = (long long)(((__int128)r * (__int128)rc.decDp[i - 1] + half) >> 53);
-  return (int)(Fi - (long long)rc.D * Fp);
 }
 
 __device__ __forceinline__ uint32_t lift_signed(int d, uint32_t p) {
@@ -82,82 +102,109 @@ __device__ __forceinline__ uint32_t lift_signed(int d, uint32_t p) {
 }
 
 // ---------------------------------------------------------------------------
-// radix-T cyclic stages shared by the forward/inverse transforms
+// transform building blocks over nb buffers of N words each (block-wide)
 
-// forward DIF stages s = 0 .. alpha-3 (all but the last, L > 1) on nb buffers
-template <int T, int PR>
-__device__ void fwd_mid_stages(uint32_t* buf, int nb, const RingConst& rc, const uint32_t* wt) {
+// forward first step, in place: buf[q-1][m] = omega^{q m} sum_{j<T-1} zeta^{q j} buf[j][m]
+template <int T, int A, int PR>
+__device__ __forceinline__ void fwd_first_step(uint32_t* buf, int nb, const RingConst& rc,
+                                               const uint32_t* wt) {
   const PrimeConst& pc = rc.pc[PR];
-  const int n1 = rc.n1, nsub = n1 / T;
-  int L = nsub;
-  for (int s = 0; s < rc.alpha - 2; ++s, L /= T) {
-    const int step = rc.M / (T * L);
-    for (int it = threadIdx.x; it < rc.nitems; it += blockDim.x) {
+  const Geo<T, A> g(rc);
+  for (int w = threadIdx.x; w < g.n1 * nb; w += blockDim.x) {
+    const int i = w / g.n1, m = w - i * g.n1;
+    uint32_t* v = buf + i * g.N + m;
+    uint32_t vals[T - 1];
+#pragma unroll
+    for (int j = 0; j < T - 1; ++j) vals[j] = v[j * g.n1];
+#pragma unroll
+    for (int q = 1; q < T; ++q) {
+      uint64_t s = 0;
+#pragma unroll
+      for (int j = 0; j < T - 1; ++j) s += (uint64_t)vals[j] * pc.z[q][j];
+      v[(q - 1) * g.n1] = mont_mul(redc(s, pc.p, pc.pinv), wt[q * m], pc.p, pc.pinv);
+    }
+  }
+  __syncthreads();
+}
+
+// forward DIF stages s = 0 .. alpha-3 (all but the last, span > 1)
+template <int T, int A, int PR>
+__device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const RingConst& rc,
+                                               const uint32_t* wt) {
+  const PrimeConst& pc = rc.pc[PR];
+  const Geo<T, A> g(rc);
+  const int nsub = g.n1 / T;
+#pragma unroll
+  for (int s = 0; s < (A ? A - 2 : 16); ++s) {
+    if (!A && s >= g.alpha - 2) break;
+    const int L = A ? cpow(T, A - 2 - s) : nsub / cpow(T, s);
+    const int step = g.M / (T * L);
+    for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
+      const int q = w / g.nitems, it = w - q * g.nitems;
       const int sub = it / nsub, rem = it - sub * nsub;
       const int b = rem / L, j = rem - b * L;
-      const int base = sub * n1 + b * T * L + j;
+      uint32_t* v = buf + q * g.N + sub * g.n1 + b * T * L + j;
       const int e1 = step * j;
-      for (int q = 0; q < nb; ++q) {
-        uint32_t* v = buf + q * rc.N + base;
-        uint32_t x[T], y[T];
+      uint32_t x[T], y[T];
 #pragma unroll
-        for (int m = 0; m < T; ++m) x[m] = v[m * L];
-        dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
-        v[0] = y[0];
+      for (int m = 0; m < T; ++m) x[m] = v[m * L];
+      dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
+      v[0] = y[0];
 #pragma unroll
-        for (int k = 1; k < T; ++k) v[k * L] = mont_mul(y[k], wt[e1 * k], pc.p, pc.pinv);
-      }
+      for (int k = 1; k < T; ++k) v[k * L] = mont_mul(y[k], wt[e1 * k], pc.p, pc.pinv);
     }
     __syncthreads();
   }
 }
 
-// inverse DIT stages s = alpha-3 .. 0 (all but the first-undone L == 1 stage)
-template <int T, int PR>
-__device__ void inv_mid_stages(uint32_t* buf, int nb, const RingConst& rc, const uint32_t* wt) {
+// inverse DIT stages s = alpha-3 .. 0 (the span-1 stage is undone in registers)
+template <int T, int A, int PR>
+__device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const RingConst& rc,
+                                               const uint32_t* wt) {
   const PrimeConst& pc = rc.pc[PR];
-  const int n1 = rc.n1, nsub = n1 / T;
-  int L = T;
-  for (int s = rc.alpha - 3; s >= 0; --s, L *= T) {
-    const int step = rc.M / (T * L);
-    for (int it = threadIdx.x; it < rc.nitems; it += blockDim.x) {
+  const Geo<T, A> g(rc);
+  const int nsub = g.n1 / T;
+#pragma unroll
+  for (int si = 0; si < (A ? A - 2 : 16); ++si) {
+    if (!A && si >= g.alpha - 2) break;
+    const int L = cpow(T, si + 1);
+    const int step = g.M / (T * L);
+    for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
+      const int q = w / g.nitems, it = w - q * g.nitems;
       const int sub = it / nsub, rem = it - sub * nsub;
       const int b = rem / L, j = rem - b * L;
-      const int base = sub * n1 + b * T * L + j;
+      uint32_t* v = buf + q * g.N + sub * g.n1 + b * T * L + j;
       const int e1 = step * j;
-      for (int q = 0; q < nb; ++q) {
-        uint32_t* v = buf + q * rc.N + base;
-        uint32_t z[T], x[T];
-        z[0] = v[0];
+      uint32_t z[T], x[T];
+      z[0] = v[0];
 #pragma unroll
-        for (int k = 1; k < T; ++k) z[k] = mont_mul(v[k * L], wt[rc.M - e1 * k], pc.p, pc.pinv);
-        dft_t<T>(z, x, pc.zi, pc.p, pc.pinv);
+      for (int k = 1; k < T; ++k) z[k] = mont_mul(v[k * L], wt[g.M - e1 * k], pc.p, pc.pinv);
+      dft_t<T>(z, x, pc.zi, pc.p, pc.pinv);
 #pragma unroll
-        for (int m = 0; m < T; ++m) v[m * L] = x[m];
-      }
+      for (int m = 0; m < T; ++m) v[m * L] = x[m];
     }
     __syncthreads();
   }
 }
 
-// inverse first step: untwist + (t-1)x(t-1) solve, writes y_i in [0, p)
-template <int T, int PR>
-__device__ void inv_first_step(uint32_t* buf, int nb, const RingConst& rc, const uint32_t* wt) {
+// inverse first step: untwist + (t-1)x(t-1) solve, writes CRT-weighted y_i in [0, p)
+template <int T, int A, int PR>
+__device__ __forceinline__ void inv_first_step(uint32_t* buf, int nb, const RingConst& rc,
+                                               const uint32_t* wt) {
   const PrimeConst& pc = rc.pc[PR];
-  const int n1 = rc.n1;
-  for (int m = threadIdx.x; m < n1; m += blockDim.x) {
-    for (int q = 0; q < nb; ++q) {
-      uint32_t* v = buf + q * rc.N + m;
-      uint32_t C[T - 1];
+  const Geo<T, A> g(rc);
+  for (int w = threadIdx.x; w < g.n1 * nb; w += blockDim.x) {
+    const int q = w / g.n1, m = w - q * g.n1;
+    uint32_t* v = buf + q * g.N + m;
+    uint32_t C[T - 1];
 #pragma unroll
-      for (int r = 1; r < T; ++r) C[r - 1] = mont_mul(v[(r - 1) * n1], wt[rc.M - r * m], pc.p, pc.pinv);
+    for (int r = 1; r < T; ++r) C[r - 1] = mont_mul(v[(r - 1) * g.n1], wt[g.M - r * m], pc.p, pc.pinv);
 #pragma unroll
-      for (int j = 0; j < T - 1; ++j) {
-        uint64_t s = 0;
+    for (int j = 0; j < T - 1; ++j) {
+      uint64_t s = 0;
 #pragma unroll
-        for (int r = 0; r < T - 1; ++r) s += (uint64_t)C[r] * pc.g[j][r];
-        v[j * n1] = fully(redc(s, pc.p, pc.pinv), pc.p);
-      }
+      for (int r = 0; r < T - 1; ++r) s += (uint64_t)C[r] * pc.g[j][r];
+      v[j * g.n1] = fully(redc(s, pc.p, pc.pinv), pc.p);
     }
   }
   __syncthreads();
@@ -182,11 +229,12 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst
   return s;
 }
 
-template <int T, int L, int PR>
+template <int T, int A, int L, int PR>
 __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem) {
   const PrimeConst& pc = rc.pc[PR];
   const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
-  const int N = rc.N, n1 = rc.n1, M = rc.M;
+  const Geo<T, A> g(rc);
+  const int N = g.N, n1 = g.n1, M = g.M;
   SmemLayout S = carve(smem, rc);
   const int64_t row = blockIdx.x / rc.np;
   const uint64_t* xin = a.in + row * 2 * (int64_t)N;
@@ -196,7 +244,7 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   // stage x.a and the twiddle table; detect an all-zero row
   int nz = 0;
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    uint64_t va = xin[k], vb = xin[N + k];
+    const uint64_t va = xin[k], vb = xin[N + k];
     S.xa[k] = va;
     nz |= (va | vb) != 0;
   }
@@ -217,42 +265,27 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   if (PR == 0 && threadIdx.x == 0 && a.counter) atomicAdd(a.counter, (unsigned long long)a.nreps);
 
   const int item = threadIdx.x;
-  const bool owner = item < rc.nitems;
+  const bool owner = item < g.nitems;
 
   for (int r = 0; r < a.nreps; ++r) {
     const uint32_t dinv = a.dinv[r];
-    const uint32_t step1 = fastmod((uint32_t)n1 * dinv, M, rc.magicM);
-    // ---- forward first step with fused automorphism + per-digit decomposition ----
-    for (int m = threadIdx.x; m < n1; m += blockDim.x) {
-      const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
-      const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
-      uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
-      uint64_t y[T - 1];
+    // ---- A: automorphism gather + digits of every coefficient ----
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+      const uint32_t km = (uint32_t)(k % n1);
+      const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
+      const uint32_t s2 = fastmod((uint32_t)(N + km) * dinv, M, rc.magicM);
+      uint64_t y = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
+      if (s2 < (uint32_t)N) y -= S.xa[s2];
+      int dg[L];
+      decompose<L>(y & QMASK, dg, rc);
 #pragma unroll
-      for (int j = 0; j < T - 1; ++j) {
-        const uint64_t v1 = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
-        y[j] = (v1 - v2) & QMASK;
-        s1 += step1;
-        if (s1 >= (uint32_t)M) s1 -= M;
-      }
-#pragma unroll 1
-      for (int i = 0; i < L; ++i) {
-        uint32_t vals[T - 1];
-#pragma unroll
-        for (int j = 0; j < T - 1; ++j) vals[j] = lift_signed(digit_i(y[j], i, rc), p);
-        uint32_t* o = S.buf + i * N + m;
-#pragma unroll
-        for (int q = 1; q < T; ++q) {
-          uint64_t s = 0;
-#pragma unroll
-          for (int j = 0; j < T - 1; ++j) s += (uint64_t)vals[j] * pc.z[q][j];
-          o[(q - 1) * n1] = mont_mul(redc(s, p, pinv), S.wt[q * m], p, pinv);
-        }
-      }
+      for (int i = 0; i < L; ++i) S.buf[i * N + k] = lift_signed(dg[i], p);
     }
     __syncthreads();
-    fwd_mid_stages<T, PR>(S.buf, L, rc, S.wt);
-    // ---- last stage (span 1) in registers, MAC against the key spectra ----
+    // ---- B: first step + mid stages of the l digit transforms ----
+    fwd_first_step<T, A, PR>(S.buf, L, rc, S.wt);
+    fwd_mid_stages<T, A, PR>(S.buf, L, rc, S.wt);
+    // ---- C: last stage (span 1) in registers, MAC against the key spectra ----
     if (owner) {
       const uint32_t* ks = a.spec[r];
       uint64_t ta[T], tb[T];
@@ -269,8 +302,8 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
         const uint32_t* kb = ks + ((size_t)(i * 2 + 1) * rc.np + PR) * N + item;
 #pragma unroll
         for (int k = 0; k < T; ++k) {
-          ta[k] += (uint64_t)yv[k] * __ldg(ka + k * rc.nitems);
-          tb[k] += (uint64_t)yv[k] * __ldg(kb + k * rc.nitems);
+          ta[k] += (uint64_t)yv[k] * __ldg(ka + k * g.nitems);
+          tb[k] += (uint64_t)yv[k] * __ldg(kb + k * g.nitems);
         }
       }
       // L products of (<2p)(<p) < p 2^32 (p < 2^31/L): one REDC each; sum over reps < 2 reps p
@@ -304,8 +337,8 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
     }
   }
   __syncthreads();
-  inv_mid_stages<T, PR>(S.buf, 2, rc, S.wt);
-  inv_first_step<T, PR>(S.buf, 2, rc, S.wt);
+  inv_mid_stages<T, A, PR>(S.buf, 2, rc, S.wt);
+  inv_first_step<T, A, PR>(S.buf, 2, rc, S.wt);
 
   // ---- explicit CRT across the cluster through distributed shared memory ----
   cluster.sync();
@@ -326,10 +359,10 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
         fb += (double)yb * rc.pc[i].inv_p;
       }
     }
-    const uint64_t A = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
-    const uint64_t B = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
+    const uint64_t Av = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
+    const uint64_t Bv = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
     uint64_t bsum = a.identity ? xin[N + k] : 0ull;
-    const uint32_t kmod = fastmod((uint32_t)k, n1, rc.magicN1);
+    const uint32_t kmod = (uint32_t)(k % n1);
     for (int r = 0; r < a.nreps; ++r) {
       const uint32_t dinv = a.dinv[r];
       const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
@@ -338,65 +371,54 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
       if (s2 < (uint32_t)N) v -= xin[N + s2];
       bsum += v;
     }
-    xout[k] = ((a.identity ? S.xa[k] : 0ull) - A) & QMASK;
-    xout[N + k] = (bsum - B) & QMASK;
+    xout[k] = ((a.identity ? S.xa[k] : 0ull) - Av) & QMASK;
+    xout[N + k] = (bsum - Bv) & QMASK;
   }
   cluster.sync();
 }
 
 template <int T>
 struct StageLaunch {
-  static constexpr int kThreads = T == 7 ? 320 : 512;
+  static constexpr int kThreads = T == 7 ? 352 : 512;
   static constexpr int kMinBlocks = T == 7 ? 3 : 2;
 };
 
-template <int T, int L>
+template <int T, int A, int L>
 __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMinBlocks)
     ks_stage_kernel(const __grid_constant__ RingConst rc, const __grid_constant__ StageArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const unsigned rank = cg::this_cluster().block_rank();
   switch (rank) {
-    case 0: stage_body<T, L, 0>(rc, a, smem); break;
-    case 1: stage_body<T, L, 1>(rc, a, smem); break;
-    case 2: stage_body<T, L, 2>(rc, a, smem); break;
-    default: stage_body<T, L, 3>(rc, a, smem); break;
+    case 0: stage_body<T, A, L, 0>(rc, a, smem); break;
+    case 1: stage_body<T, A, L, 1>(rc, a, smem); break;
+    case 2: stage_body<T, A, L, 2>(rc, a, smem); break;
+    default: stage_body<T, A, L, 3>(rc, a, smem); break;
   }
 }
 
 // ---------------------------------------------------------------------------
 // key spectra precompute: forward transform of (centered) key polynomials,
 // times R, stored in the thread-owned layout [k * nitems + item].
-// One CTA per (slot, digit, comp, prime); not performance critical.
+// One CTA per (slot, digit, comp, prime); runs once per registered key set.
 
 template <int T, int PR>
 __device__ void spectra_body(const RingConst& rc, const SpecArgs a, unsigned char* smem, int job) {
   const PrimeConst& pc = rc.pc[PR];
-  const int N = rc.N, n1 = rc.n1;
+  const int N = rc.N;
   SmemLayout S = carve(smem, rc);
   const uint64_t* src = a.keys + (size_t)job * N;  // job = (slot*l + i)*2 + c
   for (int k = threadIdx.x; k <= rc.M; k += blockDim.x) S.wt[k] = a.twid[(size_t)PR * (rc.M + 1) + k];
-  __syncthreads();
-  for (int m = threadIdx.x; m < n1; m += blockDim.x) {
-    uint32_t vals[T - 1];
-#pragma unroll
-    for (int j = 0; j < T - 1; ++j) {
-      uint64_t v = src[j * n1 + m] & QMASK;
-      long long c = (long long)v;
-      if (v >= (1ull << 52)) c -= (1ll << 53);
-      long long r = c % (long long)pc.p;
-      if (r < 0) r += pc.p;
-      vals[j] = (uint32_t)r;
-    }
-#pragma unroll
-    for (int q = 1; q < T; ++q) {
-      uint64_t s = 0;
-#pragma unroll
-      for (int j = 0; j < T - 1; ++j) s += (uint64_t)vals[j] * pc.z[q][j];
-      S.buf[(q - 1) * n1 + m] = mont_mul(redc(s, pc.p, pc.pinv), S.wt[q * m], pc.p, pc.pinv);
-    }
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    const uint64_t v = src[k] & QMASK;
+    long long c = (long long)v;
+    if (v >= (1ull << 52)) c -= (1ll << 53);
+    long long r = c % (long long)pc.p;
+    if (r < 0) r += pc.p;
+    S.buf[k] = (uint32_t)r;
   }
   __syncthreads();
-  fwd_mid_stages<T, PR>(S.buf, 1, rc, S.wt);
+  fwd_first_step<T, 0, PR>(S.buf, 1, rc, S.wt);
+  fwd_mid_stages<T, 0, PR>(S.buf, 1, rc, S.wt);
   for (int it = threadIdx.x; it < rc.nitems; it += blockDim.x) {
     uint32_t x[T], y[T];
 #pragma unroll
@@ -430,11 +452,17 @@ size_t stage_smem_bytes(const RingConst& rc) {
   return (size_t)rc.N * 8 + (size_t)((rc.M + 1 + 3) & ~3) * 4 + (size_t)(2 + nb) * rc.N * 4;
 }
 
-int stage_threads(const RingConst& rc) { return ((rc.nitems + 31) / 32) * 32; }
+int stage_threads(const RingConst& rc) {
+  const int cap = rc.t == 7 ? StageLaunch<7>::kThreads : StageLaunch<5>::kThreads;
+  const int need = ((rc.nitems + 31) / 32) * 32;
+  // enough threads for one pass over the n1 first-step columns when they fit
+  const int want = ((rc.n1 + 31) / 32) * 32;
+  return want <= cap ? (want > need ? want : need) : need;
+}
 
-template <int T, int L>
-static cudaError_t launch_stage_tl(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
-  auto kern = ks_stage_kernel<T, L>;
+template <int T, int A, int L>
+static cudaError_t launch_stage_tal(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
+  auto kern = ks_stage_kernel<T, A, L>;
   const size_t smem = stage_smem_bytes(rc);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -455,26 +483,25 @@ static cudaError_t launch_stage_tl(const RingConst& rc, const StageArgs& a, cuda
   return cudaLaunchKernelEx(&cfg, kern, rc, a);
 }
 
-template <int T>
-static cudaError_t launch_stage_t(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
+template <int T, int A>
+static cudaError_t launch_stage_ta(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
   switch (rc.l) {
-    case 1: return launch_stage_tl<T, 1>(rc, a, st);
-    case 2: return launch_stage_tl<T, 2>(rc, a, st);
-    case 3: return launch_stage_tl<T, 3>(rc, a, st);
-    case 4: return launch_stage_tl<T, 4>(rc, a, st);
-    case 5: return launch_stage_tl<T, 5>(rc, a, st);
+    case 1: return launch_stage_tal<T, A, 1>(rc, a, st);
+    case 2: return launch_stage_tal<T, A, 2>(rc, a, st);
+    case 3: return launch_stage_tal<T, A, 3>(rc, a, st);
+    case 4: return launch_stage_tal<T, A, 4>(rc, a, st);
+    case 5: return launch_stage_tal<T, A, 5>(rc, a, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_stage(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.nreps == 0) return cudaSuccess;
-  switch (rc.t) {
-    case 3: return launch_stage_t<3>(rc, a, st);
-    case 5: return launch_stage_t<5>(rc, a, st);
-    case 7: return launch_stage_t<7>(rc, a, st);
-    default: return cudaErrorInvalidValue;
-  }
+  // the production rows get a compile-time tower height; everything else is generic
+  if (rc.t == 7) return rc.alpha == 4 ? launch_stage_ta<7, 4>(rc, a, st) : launch_stage_ta<7, 0>(rc, a, st);
+  if (rc.t == 5) return rc.alpha == 5 ? launch_stage_ta<5, 5>(rc, a, st) : launch_stage_ta<5, 0>(rc, a, st);
+  if (rc.t == 3) return rc.alpha == 7 ? launch_stage_ta<3, 7>(rc, a, st) : launch_stage_ta<3, 0>(rc, a, st);
+  return cudaErrorInvalidValue;
 }
 
 template <int T>
