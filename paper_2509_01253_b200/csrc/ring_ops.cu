@@ -118,14 +118,35 @@ cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream
 // exact mod 2^53 via a 31/22-bit operand split: w*x = w*x_lo + (w*x_hi) 2^31,
 // the high product only matters mod 2^22, so a 32-bit accumulator suffices.
 
-constexpr int RPG = 16;  // rows per group
+constexpr int RPG = 16;     // rows per group
+constexpr int LCHUNK = 256; // columns staged in shared memory per chunk
+constexpr int LTHREADS = 128;
 
-__global__ void __launch_bounds__(128) linear_kernel(const __grid_constant__ RingConst rc,
-                                                     const __grid_constant__ LinearArgs a) {
+__device__ __forceinline__ void mac16(uint64_t (&lo)[RPG], uint32_t (&hi)[RPG], const int4* w4, uint64_t x) {
+  const int64_t xl = (int64_t)(x & 0x7fffffffull);
+  const uint32_t xh = (uint32_t)(x >> 31);
+#pragma unroll
+  for (int q = 0; q < RPG / 4; ++q) {
+    const int4 v = w4[q];
+    lo[4 * q + 0] += (uint64_t)((int64_t)v.x * xl);
+    hi[4 * q + 0] += (uint32_t)v.x * xh;
+    lo[4 * q + 1] += (uint64_t)((int64_t)v.y * xl);
+    hi[4 * q + 1] += (uint32_t)v.y * xh;
+    lo[4 * q + 2] += (uint64_t)((int64_t)v.z * xl);
+    hi[4 * q + 2] += (uint32_t)v.z * xh;
+    lo[4 * q + 3] += (uint64_t)((int64_t)v.w * xl);
+    hi[4 * q + 3] += (uint32_t)v.w * xh;
+  }
+}
+
+__global__ void __launch_bounds__(LTHREADS) linear_kernel(const __grid_constant__ RingConst rc,
+                                                          const __grid_constant__ LinearArgs a) {
+  __shared__ int64_t colp[LCHUNK];                 // physical row offset (row * lanes) or -1
+  __shared__ __align__(16) int32_t wsm[LCHUNK * RPG];
   const int64_t g = blockIdx.x;
   const int64_t W2 = a.lanes;
   const int64_t lane = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
-  if (lane >= W2) return;
+  const bool act = lane < W2;
   const int32_t* gr = a.groups + 6 * g;
   const int c0 = gr[0], nc = gr[1], w0 = gr[2], r0 = gr[3], nr = gr[4], per = gr[5];
   uint64_t lo[RPG];
@@ -134,27 +155,38 @@ __global__ void __launch_bounds__(128) linear_kernel(const __grid_constant__ Rin
   for (int r = 0; r < RPG; ++r) { lo[r] = 0; hi[r] = 0; }
 
   if (!per) {
-    for (int c = 0; c < nc; ++c) {
-      const int col = __ldg(a.cols + c0 + c);
-      if (col < 0) continue;
-      const int64_t src = a.in_map ? __ldg(a.in_map + col) : col;
-      const uint64_t x = __ldg(a.in + src * W2 + lane);
-      const int64_t xl = (int64_t)(x & 0x7fffffffull);
-      const uint32_t xh = (uint32_t)(x >> 31);
-      const int4* wv = reinterpret_cast<const int4*>(a.weights + w0 + (int64_t)c * RPG);
-      int w[RPG];
-#pragma unroll
-      for (int q = 0; q < RPG / 4; ++q) {
-        const int4 v = __ldg(wv + q);
-        w[4 * q] = v.x; w[4 * q + 1] = v.y; w[4 * q + 2] = v.z; w[4 * q + 3] = v.w;
+    for (int cb = 0; cb < nc; cb += LCHUNK) {
+      const int cn = min(LCHUNK, nc - cb);
+      __syncthreads();
+      for (int k = threadIdx.x; k < cn; k += blockDim.x) {
+        const int col = __ldg(a.cols + c0 + cb + k);
+        colp[k] = col < 0 ? -1 : (a.in_map ? __ldg(a.in_map + col) : (int64_t)col) * W2;
       }
+      const int4* wsrc = reinterpret_cast<const int4*>(a.weights + w0 + (int64_t)cb * RPG);
+      int4* wdst = reinterpret_cast<int4*>(wsm);
+      for (int k = threadIdx.x; k < cn * (RPG / 4); k += blockDim.x) wdst[k] = __ldg(wsrc + k);
+      __syncthreads();
+      if (act) {
+        int k = 0;
+        for (; k + 4 <= cn; k += 4) {
+          uint64_t x[4];
 #pragma unroll
-      for (int r = 0; r < RPG; ++r) {
-        lo[r] += (uint64_t)((int64_t)w[r] * xl);
-        hi[r] += (uint32_t)w[r] * xh;
+          for (int u = 0; u < 4; ++u) {
+            const int64_t off = colp[k + u];
+            x[u] = off >= 0 ? __ldg(a.in + off + lane) : 0ull;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            mac16(lo, hi, reinterpret_cast<const int4*>(wsm + (k + u) * RPG), x[u]);
+        }
+        for (; k < cn; ++k) {
+          const int64_t off = colp[k];
+          const uint64_t x = off >= 0 ? __ldg(a.in + off + lane) : 0ull;
+          mac16(lo, hi, reinterpret_cast<const int4*>(wsm + k * RPG), x);
+        }
       }
     }
-  } else {
+  } else if (act) {
 #pragma unroll
     for (int r = 0; r < RPG; ++r) {
       if (r < nr) {
@@ -170,6 +202,7 @@ __global__ void __launch_bounds__(128) linear_kernel(const __grid_constant__ Rin
       }
     }
   }
+  if (!act) return;
 
 #pragma unroll
   for (int r = 0; r < RPG; ++r) {
@@ -196,8 +229,8 @@ __global__ void __launch_bounds__(128) linear_kernel(const __grid_constant__ Rin
 
 cudaError_t launch_linear(const RingConst& rc, const LinearArgs& a, cudaStream_t st) {
   if (a.G == 0) return cudaSuccess;
-  dim3 grid((unsigned)a.G, (unsigned)((a.lanes + 127) / 128));
-  linear_kernel<<<grid, 128, 0, st>>>(rc, a);
+  dim3 grid((unsigned)a.G, (unsigned)((a.lanes + LTHREADS - 1) / LTHREADS));
+  linear_kernel<<<grid, LTHREADS, 0, st>>>(rc, a);
   return cudaGetLastError();
 }
 
