@@ -12,7 +12,9 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libsfhr_b200.so"
+import os
+
+LIB_PATH = Path(os.environ.get("SFHR_LIB_PATH") or Path(__file__).resolve().parent / "libsfhr_b200.so")
 
 SFHR_OK, SFHR_EINVAL, SFHR_EKEY, SFHR_ECUDA, SFHR_EMODEL, SFHR_ENOMEM = range(6)
 

@@ -54,6 +54,30 @@ def _compile(src: str, verbose: bool) -> Path:
     return out
 
 
+def build_variant(name: str, defines: dict) -> Path:
+    """Experimental build with -D macros into lib<name>.so (A/B kernel studies)."""
+    out_dir = OBJ / name
+    out_dir.mkdir(parents=True, exist_ok=True)
+    flags = [f"-D{k}={v}" for k, v in defines.items()]
+
+    def comp(src):
+        o = out_dir / (src + ".o")
+        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *flags, "-c", str(CSRC / src), "-o", str(o)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(r.stderr)
+        return o
+
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(comp, SOURCES))
+    lib = PKG / f"lib{name}.so"
+    r = subprocess.run([_nvcc(), *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    return lib
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     if force:

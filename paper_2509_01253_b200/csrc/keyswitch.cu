@@ -33,6 +33,10 @@
 #include "sfhr_common.cuh"
 #include "sfhr_kernels.h"
 
+#ifndef SFHR_FUSED_FIRST_STEP
+#define SFHR_FUSED_FIRST_STEP 1
+#endif
+
 namespace cg = cooperative_groups;
 
 namespace sfhr {
@@ -269,6 +273,45 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
 
   for (int r = 0; r < a.nreps; ++r) {
     const uint32_t dinv = a.dinv[r];
+#if SFHR_FUSED_FIRST_STEP
+    // ---- A+B fused: per column m, gather the T-1 coefficients j*n1+m of
+    // aut(x.a), decompose them (carry chain, all digits), and run the first
+    // transform step for every digit straight from registers ----
+    {
+      const uint32_t step1 = fastmod((uint32_t)n1 * dinv, M, rc.magicM);
+      for (int m = threadIdx.x; m < n1; m += blockDim.x) {
+        const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
+        const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
+        uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
+        int dg[L][T - 1];
+#pragma unroll
+        for (int j = 0; j < T - 1; ++j) {
+          const uint64_t v1 = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
+          int d[L];
+          decompose<L>((v1 - v2) & QMASK, d, rc);
+#pragma unroll
+          for (int i = 0; i < L; ++i) dg[i][j] = d[i];
+          s1 += step1;
+          if (s1 >= (uint32_t)M) s1 -= M;
+        }
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          uint32_t vals[T - 1];
+#pragma unroll
+          for (int j = 0; j < T - 1; ++j) vals[j] = lift_signed(dg[i][j], p);
+          uint32_t* o = S.buf + i * N + m;
+#pragma unroll
+          for (int q = 1; q < T; ++q) {
+            uint64_t s = 0;
+#pragma unroll
+            for (int j = 0; j < T - 1; ++j) s += (uint64_t)vals[j] * pc.z[q][j];
+            o[(q - 1) * n1] = mont_mul(redc(s, p, pinv), S.wt[q * m], p, pinv);
+          }
+        }
+      }
+      __syncthreads();
+    }
+#else
     // ---- A: automorphism gather + digits of every coefficient ----
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
       const uint32_t km = (uint32_t)(k % n1);
@@ -284,6 +327,7 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
     __syncthreads();
     // ---- B: first step + mid stages of the l digit transforms ----
     fwd_first_step<T, A, PR>(S.buf, L, rc, S.wt);
+#endif
     fwd_mid_stages<T, A, PR>(S.buf, L, rc, S.wt);
     // ---- C: last stage (span 1) in registers, MAC against the key spectra ----
     if (owner) {
@@ -377,10 +421,13 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   cluster.sync();
 }
 
+#ifndef SFHR_T7_MINBLOCKS
+#define SFHR_T7_MINBLOCKS 3
+#endif
 template <int T>
 struct StageLaunch {
   static constexpr int kThreads = T == 7 ? 352 : 512;
-  static constexpr int kMinBlocks = T == 7 ? 3 : 2;
+  static constexpr int kMinBlocks = T == 7 ? SFHR_T7_MINBLOCKS : 2;
 };
 
 template <int T, int A, int L>
