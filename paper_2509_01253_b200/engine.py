@@ -309,10 +309,14 @@ class ServerEngine:
         return packed, st
 
     def round_device(self, round_no: int, key: DeviceKey, power, exps, in_map, out_map,
-                     timed: bool = True):
+                     timed: bool = True, groups: Optional[tuple] = None, counter=None):
         """Device part of one round. power: host (k, npow, 2, N) uint64 or device tensor;
         in_map / out_map: device int64 tensors (out_map None for the final round).
 
+        groups=(g0, g1) packs only that range of pack groups (multi-GPU sharding,
+        SURVEY §8(e)); extraction and the linear map are computed in full.
+        counter: optional device int64 accumulator; when given the call does not
+        synchronise and returns key_switches=None (the caller reads the counter).
         Returns (packs_dev, key_switches, (extract_s, linear_s, pack_s)).
         """
         rnd = self.model.rounds[round_no - 1]
@@ -327,14 +331,19 @@ class ServerEngine:
         if ev:
             ev[1].record(stream)
         G = -(-rnd.output_len // F)
-        buf = torch.zeros((G * F, 2, ctx.N), dtype=torch.int64, device=self.dev)
+        buf = torch.empty((G * F, 2, ctx.N), dtype=torch.int64, device=self.dev)
+        if G * F > rnd.output_len:
+            buf[rnd.output_len:].zero_()  # zero padding of the last group (protocol.py:300-303)
         run_round(ctx, self._passes[round_no - 1], rows, in_map, buf, out_map, self._bias_unit)
         if ev:
             ev[2].record(stream)
-        cnt = ctx.counter()
-        packs = pack_device(ctx, key, buf, G, cnt, skip_zero=True)
+        cnt = ctx.counter() if counter is None else counter
+        g0, g1 = (0, G) if groups is None else groups
+        packs = pack_device(ctx, key, buf[g0 * F:g1 * F], g1 - g0, cnt, skip_zero=True)
         if ev:
             ev[3].record(stream)
+        if counter is not None:
+            return packs, None, (0.0, 0.0, 0.0)
         nks = int(cnt.item())  # synchronises the stream
         times = (0.0, 0.0, 0.0)
         if ev:
