@@ -117,8 +117,19 @@ typedef struct {
   const uint64_t* unit;      /* (N,) bias unit payload, tracepack.py:157-172 */
   int64_t lanes;             /* u64 lanes per row; 0 = 2N (ciphertext rows) */
   int64_t body_off;          /* first lane receiving bias*unit (N for ciphertext rows) */
+  /* Optional tensor-core tile groups (tcgen05 kind::i8; |w| <= 127): output
+   * rows of consecutive shared-column groups merged into tiles of <= 256 rows.
+   * The groups above must then exclude those rows. */
+  const int32_t* mma_tiles;  /* (n_mma_tiles, 8): cols_off, K_pad, w_off, rows_off, nrows, N_pad, 0, 0 */
+  int64_t n_mma_tiles;
+  const int32_t* mma_cols;   /* K_pad input-column indices per tile (-1 = zero tap) */
+  const int32_t* mma_rows;   /* canonical output row of each tile row */
+  const uint8_t* mma_w;      /* packed s8 weights, UMMA K-major no-swizzle core matrices */
+  int32_t mma_max_np, mma_max_kp;  /* largest N_pad / K_pad over the tiles */
 } sfhr_linear_desc;
 int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* desc, void* stream);
+/* sizeof(sfhr_linear_desc), for binding-layout checks */
+size_t sfhr_linear_desc_bytes(void);
 
 /* ServerEngine._pack / tracepack.pack_rows + fast_pack (reference
  * protocol.py:296-321, tracepack.py:288-348) for n_groups zero-padded groups

@@ -35,6 +35,7 @@ def _load() -> C.CDLL:
         "sfhr_ctx_destroy": (i32, [vp]),
         "sfhr_ctx_info": (i32, [vp, C.POINTER(C.c_int64), i32]),
         "sfhr_ringconst_bytes": (sz, []),
+        "sfhr_linear_desc_bytes": (sz, []),
         "sfhr_ctx_debug_tables": (i32, [vp, vp, sz, vp, sz]),
         "sfhr_ctx_dual": (i32, [vp, vp, vp, vp]),
         "sfhr_register_ksk": (i32, [vp, vp, i32, vp, vp, C.POINTER(vp)]),
@@ -98,7 +99,10 @@ class LinearDesc(C.Structure):
                [("n_groups", C.c_int64)] + \
                [(n, C.c_void_p) for n in ("cols", "weights", "rows", "ex_ptr", "ex_col", "ex_w",
                                          "bias", "unit")] + \
-               [("lanes", C.c_int64), ("body_off", C.c_int64)]
+               [("lanes", C.c_int64), ("body_off", C.c_int64)] + \
+               [("mma_tiles", C.c_void_p), ("n_mma_tiles", C.c_int64)] + \
+               [(n, C.c_void_p) for n in ("mma_cols", "mma_rows", "mma_w")] + \
+               [("mma_max_np", C.c_int32), ("mma_max_kp", C.c_int32)]
 
 
 # -- mirrors of the device constant block (debug / CPU verification only) --
@@ -117,6 +121,7 @@ class RingConst(C.Structure):
 
 
 assert C.sizeof(RingConst) == lib.sfhr_ringconst_bytes(), "RingConst layout mismatch"
+assert C.sizeof(LinearDesc) == lib.sfhr_linear_desc_bytes(), "sfhr_linear_desc layout mismatch"
 
 
 def ptr(a) -> int | None:

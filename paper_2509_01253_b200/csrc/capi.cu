@@ -250,6 +250,8 @@ int sfhr_ctx_debug_tables(const sfhr_ctx* ctx, void* ringconst, size_t rc_bytes,
 
 size_t sfhr_ringconst_bytes(void) { return sizeof(RingConst); }
 
+size_t sfhr_linear_desc_bytes(void) { return sizeof(sfhr_linear_desc); }
+
 int sfhr_ctx_dual(const sfhr_ctx* ctx, int32_t* e1, int32_t* e2, int32_t* ratio_len) {
   if (!ctx) return fail(SFHR_EINVAL, "null context");
   const Plan& P = ctx->plan;
@@ -401,6 +403,38 @@ int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* d, void* stream) {
   if (a.lanes > 65535LL * 128) return fail(SFHR_EINVAL, "too many lanes per row");
   CK(launch_linear(ctx->plan.rc, a, (cudaStream_t)stream), "linear kernel");
   if (a.G) ++g_launches;
+  if (d->n_mma_tiles > 0) {
+    if (!d->mma_tiles || !d->mma_cols || !d->mma_rows || !d->mma_w)
+      return fail(SFHR_EINVAL, "incomplete tensor-core tile description");
+    LinearMmaArgs m;
+    m.in = a.in;
+    m.in_map = a.in_map;
+    m.round_in = a.round_in;
+    m.round_map = a.round_map;
+    m.out = a.out;
+    m.out_map = a.out_map;
+    m.tiles = d->mma_tiles;
+    m.tcols = d->mma_cols;
+    m.trows = d->mma_rows;
+    m.tw = d->mma_w;
+    m.ex_ptr = a.ex_ptr;
+    m.ex_col = a.ex_col;
+    m.ex_w = a.ex_w;
+    m.bias = a.bias;
+    m.unit = a.unit;
+    m.T = d->n_mma_tiles;
+    m.lanes = a.lanes;
+    m.body_off = a.body_off;
+    // M-tiles per CTA: enough CTAs to fill the GPU several times, <= 16 tiles so the
+    // column slice all tile groups of a wave touch stays L2-resident
+    const int64_t n_mt = (a.lanes + 15) / 16;
+    int64_t per = (m.T * n_mt + 148 * 8 - 1) / (148 * 8);
+    per = per < 1 ? 1 : (per > 16 ? 16 : per);
+    const int64_t chunks = (n_mt + per - 1) / per;
+    m.mt_per_cta = (int)((n_mt + chunks - 1) / chunks);
+    CK(launch_linear_mma(m, d->mma_max_np, d->mma_max_kp, (cudaStream_t)stream), "linear tensor-core kernel");
+    ++g_launches;
+  }
   return SFHR_OK;
 }
 

@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(512) ks_spectra_kernel(const __grid_constant__
 // ---------------------------------------------------------------------------
 // launchers
 
+#if !defined(SFHR_KS_T)
 size_t stage_smem_bytes(const RingConst& rc) {
   const int nb = rc.l > 2 ? rc.l : 2;
   return (size_t)rc.N * 8 + (size_t)((rc.M + 1 + 3) & ~3) * 4 + (size_t)(2 + nb) * rc.N * 4;
@@ -506,6 +507,7 @@ int stage_threads(const RingConst& rc) {
   const int want = ((rc.n1 + 31) / 32) * 32;
   return want <= cap ? (want > need ? want : need) : need;
 }
+#endif
 
 template <int T, int A, int L>
 static cudaError_t launch_stage_tal(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
@@ -530,24 +532,43 @@ static cudaError_t launch_stage_tal(const RingConst& rc, const StageArgs& a, cud
   return cudaLaunchKernelEx(&cfg, kern, rc, a);
 }
 
-template <int T, int A>
-static cudaError_t launch_stage_ta(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
-  switch (rc.l) {
-    case 1: return launch_stage_tal<T, A, 1>(rc, a, st);
-    case 2: return launch_stage_tal<T, A, 2>(rc, a, st);
-    case 3: return launch_stage_tal<T, A, 3>(rc, a, st);
-    case 4: return launch_stage_tal<T, A, 4>(rc, a, st);
-    case 5: return launch_stage_tal<T, A, 5>(rc, a, st);
-    default: return cudaErrorInvalidValue;
-  }
+// One translation unit per (t, l) (build.py compiles this file with
+// -DSFHR_KS_T=t -DSFHR_KS_L=l) keeps the template fan-out compiling in parallel.
+#define SFHR_KS_DECL(T, L) \
+  cudaError_t launch_stage_t##T##_l##L(const RingConst& rc, const StageArgs& a, cudaStream_t st)
+#define SFHR_KS_DECL_ALL(T) SFHR_KS_DECL(T, 1); SFHR_KS_DECL(T, 2); SFHR_KS_DECL(T, 3); \
+  SFHR_KS_DECL(T, 4); SFHR_KS_DECL(T, 5);
+SFHR_KS_DECL_ALL(3)
+SFHR_KS_DECL_ALL(5)
+SFHR_KS_DECL_ALL(7)
+
+#if defined(SFHR_KS_T) && defined(SFHR_KS_L)
+#define SFHR_CAT2(a, b, c, d) a##b##c##d
+#define SFHR_CAT(a, b, c, d) SFHR_CAT2(a, b, c, d)
+// the production rows get a compile-time tower height; everything else is generic
+cudaError_t SFHR_CAT(launch_stage_t, SFHR_KS_T, _l, SFHR_KS_L)(const RingConst& rc, const StageArgs& a,
+                                                              cudaStream_t st) {
+  constexpr int T = SFHR_KS_T, L = SFHR_KS_L;
+  constexpr int A = T == 7 ? 4 : T == 5 ? 5 : 7;
+  return rc.alpha == A ? launch_stage_tal<T, A, L>(rc, a, st) : launch_stage_tal<T, 0, L>(rc, a, st);
 }
+#else
+
+#define SFHR_KS_CASES(T)                              \
+  switch (rc.l) {                                     \
+    case 1: return launch_stage_t##T##_l1(rc, a, st); \
+    case 2: return launch_stage_t##T##_l2(rc, a, st); \
+    case 3: return launch_stage_t##T##_l3(rc, a, st); \
+    case 4: return launch_stage_t##T##_l4(rc, a, st); \
+    case 5: return launch_stage_t##T##_l5(rc, a, st); \
+    default: return cudaErrorInvalidValue;            \
+  }
 
 cudaError_t launch_stage(const RingConst& rc, const StageArgs& a, cudaStream_t st) {
   if (a.B == 0 || a.nreps == 0) return cudaSuccess;
-  // the production rows get a compile-time tower height; everything else is generic
-  if (rc.t == 7) return rc.alpha == 4 ? launch_stage_ta<7, 4>(rc, a, st) : launch_stage_ta<7, 0>(rc, a, st);
-  if (rc.t == 5) return rc.alpha == 5 ? launch_stage_ta<5, 5>(rc, a, st) : launch_stage_ta<5, 0>(rc, a, st);
-  if (rc.t == 3) return rc.alpha == 7 ? launch_stage_ta<3, 7>(rc, a, st) : launch_stage_ta<3, 0>(rc, a, st);
+  if (rc.t == 7) SFHR_KS_CASES(7)
+  if (rc.t == 5) SFHR_KS_CASES(5)
+  if (rc.t == 3) SFHR_KS_CASES(3)
   return cudaErrorInvalidValue;
 }
 
@@ -570,5 +591,7 @@ cudaError_t launch_spectra(const RingConst& rc, const SpecArgs& a, int njobs, cu
     default: return cudaErrorInvalidValue;
   }
 }
+
+#endif  // SFHR_KS_T
 
 }  // namespace sfhr

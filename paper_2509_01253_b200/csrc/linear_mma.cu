@@ -1,0 +1,315 @@
+// Tensor-core grouped linear map over ciphertext rows (reference
+// pkg/src/sfhr/model.py:384-429 semantics): out[o] = sum_k W[o,k] * in[col_k]
+// mod 2^53, exact, on the 5th-generation tensor cores (tcgen05.mma kind::i8).
+//
+// The trick that makes a 53-bit modular MAC a plain int8 GEMM with no operand
+// transposition: view every u64 lane of an input row as its 8 little-endian
+// bytes.  With the byte-lanes of one 128-byte row slice on the MMA's M axis
+// (A operand MN-major: a tap's 128 contiguous bytes are one K-row of A), the
+// taps on K and the output rows of a tile group on N (B = s8 weights,
+// K-major), the accumulator D[m = 8u + j][o] = sum_k W[o,k] * byte_j(in_k[u])
+// is an exact s32 (|W| <= 127, K * 127 * 255 < 2^31), and
+//     out[o][u] = sum_j D[8u + j][o] << 8j   (mod 2^64, then & (2^53 - 1))
+// is the exact reference result.  Byte 7 of a lane is always 0 (values
+// < 2^53), so 7/8 of the tensor work is useful.
+//
+// Per CTA: one tile group (<= 256 output rows sharing one column list) over a
+// contiguous range of 128-byte M-tiles.  Pipeline: all 128 threads gather the
+// K taps of the next stages with cp.async (16 B, zero-fill for padding taps
+// and row tails) straight into the 128B-swizzled canonical layout; one thread
+// issues the MMAs (K = 32 each) into a double-buffered TMEM accumulator and
+// commits to per-stage mbarriers; the epilogue of tile t-1 (tcgen05.ld ->
+// smem transpose -> byte recombination, residual extras, bias*unit, sigma_r
+// scatter) runs while tile t's MMAs are in flight.
+#include "sfhr_common.cuh"
+#include "sfhr_kernels.h"
+
+namespace sfhr {
+
+namespace {
+
+constexpr int MMA_THREADS = 128;
+constexpr int KC = 64;                    // taps per pipeline stage (2 MMAs)
+constexpr int NSTAGE = 4;
+constexpr int STAGE_BYTES = KC * 128;     // 8 KB
+constexpr int EP_COLS = 16;               // accumulator columns per epilogue chunk
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint32_t nbytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(nbytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
+// UMMA shared-memory descriptor (sm_100): start, LBO, SBO in 16-byte units,
+// version 1, layout type in bits 61-63 (0 = no swizzle, 2 = 128B swizzle).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | ((uint64_t)layout << 61);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t sx(int v) { return (uint64_t)(int64_t)v; }
+
+}  // namespace
+
+// byte offsets of the dynamic shared-memory carve-up (host and device agree)
+struct MmaSmem {
+  int ring, b, ep, colp, odst, ocan, bars, tslot, total;
+  __host__ __device__ static MmaSmem make(int Np, int Kp) {
+    MmaSmem s;
+    s.ring = 0;
+    s.b = s.ring + NSTAGE * STAGE_BYTES;
+    s.ep = s.b + ((Np * Kp + 127) & ~127);
+    s.colp = s.ep + EP_COLS * 128 * 4;
+    s.odst = s.colp + Kp * 8;
+    s.ocan = s.odst + Np * 8;
+    s.bars = (s.ocan + Np * 4 + 7) & ~7;
+    s.tslot = s.bars + (NSTAGE + 2) * 8;
+    s.total = s.tslot + 16 + 1024;  // + alignment slack for the 1024-B swizzle atoms
+    return s;
+  }
+};
+
+__global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_constant__ LinearMmaArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tg = (int)(blockIdx.x % a.T);
+  const int chunk = (int)(blockIdx.x / a.T);
+  const int32_t* td = a.tiles + 8 * (int64_t)tg;
+  const int c0 = td[0], Kp = td[1], w0 = td[2], r0 = td[3], nr = td[4], Np = td[5];
+  const int64_t lanes = a.lanes;
+  const int64_t rowbytes = lanes * 8;
+  const int n_mt = (int)((lanes + 15) / 16);
+  const int mt0 = chunk * a.mt_per_cta;
+  const int mt1 = min(n_mt, mt0 + a.mt_per_cta);
+  if (mt0 >= mt1) return;
+
+  const uint32_t raw = su32(smem_raw);
+  unsigned char* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  const MmaSmem L = MmaSmem::make(Np, Kp);
+  const uint32_t ring = su32(sm + L.ring), bsm = su32(sm + L.b);
+  int32_t* ep = reinterpret_cast<int32_t*>(sm + L.ep);
+  int64_t* colp = reinterpret_cast<int64_t*>(sm + L.colp);
+  int64_t* odst = reinterpret_cast<int64_t*>(sm + L.odst);
+  int32_t* ocan = reinterpret_cast<int32_t*>(sm + L.ocan);
+  const uint32_t bars = su32(sm + L.bars);  // [0, NSTAGE): stage free; NSTAGE + {0,1}: accumulator ready
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L.tslot);
+  const uint32_t ncols = 2 * Np <= 32 ? 32 : 2 * Np <= 64 ? 64 : 2 * Np <= 128 ? 128 : 2 * Np <= 256 ? 256 : 512;
+
+  // ---- setup: B operand (weights), tap offsets, output row maps, barriers, TMEM ----
+  const unsigned char* wsrc = a.tw + w0;
+  for (int i = tid; i < Np * Kp / 16; i += MMA_THREADS) cp16(bsm + 16 * i, wsrc + 16 * i, 16);
+  cp_commit();
+  for (int k = tid; k < Kp; k += MMA_THREADS) {
+    const int col = a.tcols[c0 + k];
+    colp[k] = col < 0 ? -1 : (a.in_map ? a.in_map[col] : (int64_t)col) * rowbytes;
+  }
+  for (int o = tid; o < Np; o += MMA_THREADS) {
+    if (o < nr) {
+      const int r = a.trows[r0 + o];
+      ocan[o] = r;
+      odst[o] = a.out_map ? a.out_map[r] : (int64_t)r;
+    } else {
+      ocan[o] = -1;
+      odst[o] = -1;
+    }
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NSTAGE + 2; ++i) mbar_init(bars + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tslot)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  cp_wait<0>();
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  // kind::i8, D = s32, A = u8 (MN-major), B = s8 (K-major), M = 128, N = Np
+  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(Np >> 3) << 17) |
+                         ((128u >> 4) << 24);
+  const int nkc = (Kp + KC - 1) / KC;
+  const int total = (mt1 - mt0) * nkc;
+  const uint32_t b_kblock = (uint32_t)(Np / 8) * 128;  // bytes per 16-byte K block of B
+
+  auto issue = [&](int it) {
+    const int mt = mt0 + it / nkc, kc = it - (it / nkc) * nkc;
+    const uint32_t dst0 = ring + (it % NSTAGE) * STAGE_BYTES;
+    const int ntaps = min(KC, Kp - kc * KC);
+    const int64_t boff = (int64_t)mt * 128;
+    for (int q = tid; q < ntaps * 8; q += MMA_THREADS) {
+      const int tap = q >> 3, c = q & 7;
+      const int64_t cpos = colp[kc * KC + tap];
+      const int64_t off = boff + c * 16;
+      const bool ok = cpos >= 0 && off < rowbytes;
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.in) + (ok ? cpos + off : 0);
+      cp16(dst0 + tap * 128 + ((c ^ (tap & 7)) << 4), src, ok ? 16u : 0u);
+    }
+  };
+
+  auto epilogue = [&](int mtl) {
+    const int buf = mtl & 1;
+    mbar_wait(bars + 8 * (NSTAGE + buf), (uint32_t)((mtl >> 1) & 1));
+    tc_fence_after();
+    const int64_t lane0 = (int64_t)(mt0 + mtl) * 16;
+    for (int cc = 0; cc < Np; cc += EP_COLS) {
+      uint32_t r[16];
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * Np + cc), r);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) ep[j * 128 + tid] = (int32_t)r[j];
+      __syncthreads();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int idx = tid + MMA_THREADS * h;
+        const int c = idx >> 4, u = idx & 15;
+        const int o = cc + c;
+        const int64_t ln = lane0 + u;
+        if (o < nr && ln < lanes) {
+          const int4* p = reinterpret_cast<const int4*>(ep + c * 128 + u * 8);
+          const int4 x0 = p[0], x1 = p[1];
+          uint64_t v = sx(x0.x) + (sx(x0.y) << 8) + (sx(x0.z) << 16) + (sx(x0.w) << 24) +
+                       (sx(x1.x) << 32) + (sx(x1.y) << 40) + (sx(x1.z) << 48) + (sx(x1.w) << 56);
+          const int oc = ocan[o];
+          if (a.ex_ptr) {
+            const int e0 = a.ex_ptr[oc], e1 = a.ex_ptr[oc + 1];
+            for (int e = e0; e < e1; ++e) {
+              const int col = a.ex_col[e];
+              const int64_t src = a.round_map ? a.round_map[col] : (int64_t)col;
+              v += sx(a.ex_w[e]) * (uint64_t)a.round_in[src * lanes + ln];
+            }
+          }
+          if (a.bias && ln >= a.body_off) v += (uint64_t)a.bias[oc] * a.unit[ln - a.body_off];
+          a.out[odst[o] * lanes + ln] = v & QMASK;
+        }
+      }
+      __syncthreads();
+    }
+    tc_fence_before();
+  };
+
+  // ---- main pipeline ----
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < total) issue(s);
+    cp_commit();
+  }
+  for (int it = 0; it < total; ++it) {
+    const int nx = it + NSTAGE - 1;
+    if (nx < total) {
+      if (it >= 1) mbar_wait(bars + 8 * ((it - 1) % NSTAGE), (uint32_t)(((it - 1) / NSTAGE) & 1));
+      issue(nx);
+    }
+    cp_commit();
+    cp_wait<NSTAGE - 1>();
+    fence_proxy_async();
+    __syncthreads();
+    const int mtl = it / nkc, kc = it - mtl * nkc, s = it % NSTAGE;
+    const int buf = mtl & 1;
+    if (tid == 0) {
+      tc_fence_after();
+      const int nmma = min(KC, Kp - kc * KC) / 32;
+      for (int j = 0; j < nmma; ++j) {
+        const uint64_t ad = sdesc(ring + s * STAGE_BYTES + j * 4096, 16, 1024, 2);
+        const int kb = (kc * KC + j * 32) >> 4;
+        const uint64_t bd = sdesc(bsm + kb * b_kblock, b_kblock, 128, 0);
+        mma_i8(tmem + (uint32_t)(buf * Np), ad, bd, idesc, (kc > 0 || j > 0) ? 1u : 0u);
+      }
+      mma_commit(bars + 8 * s);
+      if (kc == nkc - 1) mma_commit(bars + 8 * (NSTAGE + buf));
+    }
+    __syncwarp();
+    if (kc == nkc - 1 && mtl > 0) epilogue(mtl - 1);
+  }
+  epilogue(mt1 - mt0 - 1);
+
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols) : "memory");
+}
+
+size_t linear_mma_smem_bytes(int Np, int Kp) {
+  return (size_t)MmaSmem::make(Np, Kp).total;
+}
+
+cudaError_t launch_linear_mma(const LinearMmaArgs& a, int max_np, int max_kp, cudaStream_t st) {
+  if (a.T == 0) return cudaSuccess;
+  if (max_np < 16 || max_np > 256 || (max_np & 15) || (max_kp & 31) || a.lanes <= 0 || (a.lanes & 1))
+    return cudaErrorInvalidValue;
+  size_t smem = linear_mma_smem_bytes(max_np, max_kp);
+  // keep resident CTAs x TMEM columns <= 512 (otherwise tcgen05.alloc would serialise)
+  const int ncols = 2 * max_np <= 32 ? 32 : 2 * max_np <= 64 ? 64 : 2 * max_np <= 128 ? 128 : 2 * max_np <= 256 ? 256 : 512;
+  const size_t floor_bytes = (size_t)(228 * 1024) / (size_t)(512 / ncols + 1) + 1024;
+  if (smem < floor_bytes) smem = floor_bytes;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(linear_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t n_mt = (a.lanes + 15) / 16;
+  const int64_t chunks = (n_mt + a.mt_per_cta - 1) / a.mt_per_cta;
+  const int64_t grid = chunks * a.T;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+  linear_mma_kernel<<<(unsigned)grid, MMA_THREADS, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sfhr

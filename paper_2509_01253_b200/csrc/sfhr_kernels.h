@@ -76,4 +76,29 @@ struct LinearArgs {
 };
 cudaError_t launch_linear(const RingConst& rc, const LinearArgs& a, cudaStream_t st);
 
+// tensor-core (tcgen05 kind::i8) variant over tile groups (linear_mma.cu)
+struct LinearMmaArgs {
+  const uint64_t* in;
+  const int64_t* in_map;
+  const uint64_t* round_in;
+  const int64_t* round_map;
+  uint64_t* out;
+  const int64_t* out_map;
+  const int32_t* tiles;      // (T, 8): cols_off, K_pad, w_off (bytes), rows_off, nrows, N_pad, 0, 0
+  const int32_t* tcols;      // K_pad column indices per tile (-1 = zero tap)
+  const int32_t* trows;      // canonical output rows per tile
+  const uint8_t* tw;         // packed s8 B operands (UMMA K-major, no swizzle)
+  const int32_t* ex_ptr;
+  const int32_t* ex_col;
+  const int32_t* ex_w;
+  const int64_t* bias;
+  const uint64_t* unit;
+  int64_t T;
+  int64_t lanes;
+  int64_t body_off;
+  int mt_per_cta;            // 128-byte M-tiles per CTA
+};
+size_t linear_mma_smem_bytes(int Np, int Kp);
+cudaError_t launch_linear_mma(const LinearMmaArgs& a, int max_np, int max_kp, cudaStream_t st);
+
 }  // namespace sfhr

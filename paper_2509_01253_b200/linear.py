@@ -10,6 +10,9 @@ protocol.py:243-254) and whose last pass scatters through sigma_r
 
 from __future__ import annotations
 
+import os
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
@@ -18,22 +21,126 @@ from .device import RingContext, to_dev, to_host_u64
 from .model import ROWS_PER_GROUP, LinearPass, ModelError
 
 _LIMB = 18
+MMA_MAX_ROWS = 256      # N of one tcgen05 tile group
+MMA_MAX_BYTES = 150 * 1024  # s8 weights of a tile group kept in shared memory
+MMA_ENABLED = os.environ.get("SFHR_LINEAR_MMA", "1") != "0"
+
+
+@dataclass
+class MmaTiles:
+    """Tensor-core tile groups of a pass (csrc/linear_mma.cu).
+
+    tiles: (T, 8) int32 [cols_off, K_pad, w_off, rows_off, nrows, N_pad, 0, 0];
+    cols: K_pad input columns per tile (-1 = zero tap); rows: canonical output
+    rows; w: s8 weights packed as UMMA K-major core matrices (8 rows x 16 B).
+    """
+    tiles: np.ndarray
+    cols: np.ndarray
+    rows: np.ndarray
+    w: np.ndarray
+    max_np: int
+    max_kp: int
+
+
+def _pack_umma_k_major(wt: np.ndarray, n_pad: int, k_pad: int) -> np.ndarray:
+    """(n, k) int8 -> canonical no-swizzle K-major layout [k/16][n/8][8][16]."""
+    b = np.zeros((n_pad, k_pad), np.int8)
+    b[:wt.shape[0], :wt.shape[1]] = wt
+    return np.ascontiguousarray(b.reshape(n_pad // 8, 8, k_pad // 16, 16).transpose(2, 0, 1, 3)).reshape(-1)
+
+
+def split_mma_tiles(ps: LinearPass):
+    """Merge runs of shared-column groups into tcgen05 tile groups.
+
+    Returns (rest_group_indices, MmaTiles | None).  A run qualifies when its
+    groups share one column list (conv pixels: every output-channel chunk;
+    fc / dense: all row chunks), |w| <= 127 (s8 B operand) and the weights fit
+    in shared memory; everything else stays on the CUDA-core kernel.
+    """
+    g = ps.groups
+    G = len(g)
+    if not MMA_ENABLED or G == 0:
+        return np.arange(G), None
+    wv = ps.weights
+    rest, tiles, tcols, trows, tw = [], [], [], [], []
+    cache = {}
+    ncols = nrows = nw = 0
+    max_np = max_kp = 0
+    i = 0
+    while i < G:
+        c0, nc, w0, r0, nr, per = (int(x) for x in g[i])
+        if per or nc == 0:
+            rest.append(i)
+            i += 1
+            continue
+        cols = ps.cols[c0:c0 + nc]
+        run, tot, j = [i], nr, i + 1
+        while j < G:
+            cj, ncj, _, _, nrj, perj = (int(x) for x in g[j])
+            if perj or ncj != nc or tot + nrj > MMA_MAX_ROWS:
+                break
+            if cj != c0 and not np.array_equal(ps.cols[cj:cj + ncj], cols):
+                break
+            run.append(j)
+            tot += nrj
+            j += 1
+        k_pad = (nc + 31) // 32 * 32
+        n_pad = (tot + 15) // 16 * 16
+        key = tuple(int(g[q][2]) for q in run) + tuple(int(g[q][4]) for q in run)
+        if key in cache:
+            woff = cache[key]
+        else:
+            wt = np.concatenate([wv[int(g[q][2]):int(g[q][2]) + nc * ROWS_PER_GROUP]
+                                 .reshape(nc, ROWS_PER_GROUP)[:, :int(g[q][4])].T for q in run])
+            if np.abs(wt).max(initial=0) > 127 or n_pad * k_pad > MMA_MAX_BYTES:
+                rest.extend(run)
+                i = j
+                continue
+            woff = nw
+            packed = _pack_umma_k_major(wt.astype(np.int8), n_pad, k_pad)
+            tw.append(packed)
+            nw += packed.size
+            cache[key] = woff
+        tiles.append((ncols, k_pad, woff, nrows, tot, n_pad, 0, 0))
+        tc = np.full(k_pad, -1, np.int64)
+        tc[:nc] = cols
+        tcols.append(tc)
+        ncols += k_pad
+        trows.append(np.concatenate([ps.rows[int(g[q][3]):int(g[q][3]) + int(g[q][4])] for q in run]))
+        nrows += tot
+        max_np, max_kp = max(max_np, n_pad), max(max_kp, k_pad)
+        i = j
+    if not tiles:
+        return np.arange(G), None
+    if nw >= 2 ** 31 or ncols >= 2 ** 31:
+        return np.arange(G), None
+    return np.asarray(rest, np.int64), MmaTiles(
+        np.asarray(tiles, np.int32).reshape(-1, 8), np.concatenate(tcols).astype(np.int32),
+        np.concatenate(trows).astype(np.int32), np.concatenate(tw), max_np, max_kp)
 
 
 class DevicePass:
-    """A LinearPass uploaded to one device."""
+    """A LinearPass uploaded to one device (CUDA-core groups + tcgen05 tile groups)."""
 
-    def __init__(self, ps: LinearPass, dev: torch.device):
+    def __init__(self, ps: LinearPass, dev: torch.device, lanes: int | None = None):
         self.in_len, self.out_len = ps.in_len, ps.out_len
-        self.n_groups = int(ps.groups.shape[0])
         up = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa
-        self.groups = up(ps.groups)
+        rest, mt = split_mma_tiles(ps) if lanes is None or lanes % 2 == 0 else (np.arange(len(ps.groups)), None)
+        self.n_groups = int(len(rest))
+        self.groups = up(ps.groups[rest].reshape(-1, 6)) if len(rest) else None
         self.cols = up(ps.cols)
         self.weights = up(ps.weights)
         self.rows = up(ps.rows)
         self.ex_ptr, self.ex_col, self.ex_w = up(ps.ex_ptr), up(ps.ex_col), up(ps.ex_w)
         self.bias = up(ps.bias)
         self.macs_per_lane = ps.macs_per_lane()
+        self.n_mma_tiles = 0 if mt is None else int(len(mt.tiles))
+        self.mma_tiles = self.mma_cols = self.mma_rows = self.mma_w = None
+        self.mma_max_np = self.mma_max_kp = 0
+        if mt is not None:
+            self.mma_tiles, self.mma_cols, self.mma_rows = up(mt.tiles), up(mt.cols), up(mt.rows)
+            self.mma_w = up(mt.w.view(np.uint8))
+            self.mma_max_np, self.mma_max_kp = mt.max_np, mt.max_kp
 
 
 def run_pass(ctx: RingContext, p: DevicePass, inp, in_map, round_in, round_map, out, out_map, unit,
@@ -55,6 +162,9 @@ def run_pass(ctx: RingContext, p: DevicePass, inp, in_map, round_in, round_map, 
     d.unit = nat.ptr(unit)
     d.lanes = lanes
     d.body_off = body_off
+    d.mma_tiles, d.n_mma_tiles = nat.ptr(p.mma_tiles), p.n_mma_tiles
+    d.mma_cols, d.mma_rows, d.mma_w = nat.ptr(p.mma_cols), nat.ptr(p.mma_rows), nat.ptr(p.mma_w)
+    d.mma_max_np, d.mma_max_kp = p.mma_max_np, p.mma_max_kp
     import ctypes as C
     nat.check(nat.lib.sfhr_linear_pass(ctx.h, C.byref(d), ctx.stream()))
 
@@ -105,7 +215,7 @@ def int_matmul_mod_q(w: np.ndarray, rows, device: int = 0):
     lanes = int(np.prod(x.shape[1:])) if x.dim() > 1 else 1
     out = torch.empty((e_out,) + tuple(x.shape[1:]), dtype=torch.int64, device=ctx.dev)
     if e_out and e_in:
-        p = DevicePass(_dense_pass(w), ctx.dev)
+        p = DevicePass(_dense_pass(w), ctx.dev, lanes=lanes)
         run_pass(ctx, p, x, None, x, None, out, None, None, lanes=lanes, body_off=lanes)
     elif e_out:
         out.zero_()

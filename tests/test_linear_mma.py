@@ -1,0 +1,136 @@
+"""Tensor-core (tcgen05 kind::i8) linear map: host tiling on CPU, device parity on GPU.
+
+The device kernel (csrc/linear_mma.cu) computes out[o][u] = sum_j D[8u+j][o] << 8j
+with D = (bytes of the gathered input rows) x (s8 weights).  The CPU tests
+replay exactly that decomposition in numpy from the packed operands the host
+uploads, so the packing and the byte algebra are pinned before any GPU run;
+the GPU tests compare the kernel against the CUDA-core kernel and the oracle's
+exact object-integer matmul (reference model.py:384-407)."""
+
+import numpy as np
+import pytest
+
+from conftest import has_cuda, u53
+from oracle import lowering as olo
+from paper_2509_01253_b200 import linear as lin
+from paper_2509_01253_b200 import model as mm
+from paper_2509_01253_b200 import workloads as W
+
+
+def _unpack(tw, n_pad, k_pad):
+    return tw.reshape(k_pad // 16, n_pad // 8, 8, 16).transpose(1, 2, 0, 3).reshape(n_pad, k_pad)
+
+
+def _emulate_tile(mt, t, rows_in):
+    """numpy replay of one tile group: byte-plane int8 GEMM + recombination."""
+    c0, kp, w0, r0, nr, np_, _, _ = (int(x) for x in mt.tiles[t])
+    B = _unpack(mt.w[w0:w0 + np_ * kp], np_, kp).astype(np.int64)      # (N_pad, K_pad) s8
+    cols = mt.cols[c0:c0 + kp]
+    X = np.zeros((kp,) + rows_in.shape[1:], np.uint64)
+    X[cols >= 0] = rows_in[cols[cols >= 0]]
+    Xb = X.reshape(kp, -1).view(np.uint8).reshape(kp, -1, 8).astype(np.int64)  # (K, lanes, 8 bytes)
+    D = np.einsum("ok,klj->olj", B[:nr], Xb)                            # s32-exact accumulators
+    assert np.abs(D).max(initial=0) < 2 ** 31
+    out = np.zeros(D.shape[:2], np.uint64)
+    for j in range(8):
+        out += (D[:, :, j].astype(np.int64).astype(np.uint64) << np.uint64(8 * j))
+    return mt.rows[r0:r0 + nr], out & np.uint64((1 << 53) - 1)
+
+
+PASSES = {
+    "resnet20_r1": lambda: mm.lower_round(W.resnet20_model(12, 0), 1),
+    "resnet20_r7": lambda: mm.lower_round(W.resnet20_model(12, 0), 7),
+    "resnet20_fc": lambda: mm.lower_round(W.resnet20_model(12, 0), 19),
+    "toy": lambda: mm.lower_round(W.toy_model(8, 3), 0),
+    "mlp": lambda: mm.lower_round(W.mlp_model(0), 0),
+    "dense_wide": lambda: [lin._dense_pass(np.random.default_rng(5).integers(-127, 128, (300, 45)))],
+    "dense_big_w": lambda: [lin._dense_pass(np.random.default_rng(6).integers(-500, 500, (20, 8)))],
+}
+
+
+@pytest.mark.parametrize("name", sorted(PASSES))
+def test_tiles_cover_rows_once_and_replay_exactly(name):
+    rng = np.random.default_rng(9)
+    for ps in PASSES[name]():
+        rest, mt = lin.split_mma_tiles(ps)
+        seen = []
+        for gi in rest:
+            c0, nc, w0, r0, nr, per = (int(x) for x in ps.groups[gi])
+            seen.extend(ps.rows[r0:r0 + nr].tolist())
+        if mt is not None:
+            seen.extend(mt.rows.tolist())
+            assert mt.tiles[:, 5].max() <= lin.MMA_MAX_ROWS
+            assert np.all(mt.tiles[:, 1] % 32 == 0) and np.all(mt.tiles[:, 5] % 16 == 0)
+        assert sorted(seen) == sorted(ps.rows.tolist())
+        if name == "dense_big_w":
+            assert mt is None  # |w| > 127 stays on the CUDA-core kernel
+            continue
+        if mt is None:  # per-row column lists (pooling, identity) stay on the CUDA cores
+            assert np.all(ps.groups[:, 5] == 1)
+            continue
+        # replay a few tiles against the exact dense product of the pass
+        Wd = np.zeros((ps.out_len, ps.in_len), np.int64)
+        for c0, nc, w0, r0, nr, per in ps.groups.tolist():
+            blk = ps.weights[w0:w0 + nc * 16].reshape(nc, 16)
+            for i in range(nr):
+                cl = ps.cols[c0 + (i * nc if per else 0): c0 + (i * nc if per else 0) + nc]
+                for c, col in enumerate(cl):
+                    if col >= 0:
+                        Wd[ps.rows[r0 + i], col] += blk[c, i]
+        x = rng.integers(0, 1 << 53, (ps.in_len, 2, 5), dtype=np.uint64)
+        for t in sorted({0, len(mt.tiles) // 2, len(mt.tiles) - 1}):
+            rows, got = _emulate_tile(mt, t, x)
+            want = olo.int_matmul_exact_objects(Wd[rows], x).reshape(len(rows), -1)
+            assert np.array_equal(got, want), (name, t)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("shape", [(1, 1, 2), (16, 32, 16), (17, 33, 18), (300, 45, 30), (5, 700, 2),
+                                   (64, 576, 4116), (128, 784, 100)])
+def test_mma_matmul_matches_oracle(shape):
+    e_out, e_in, lanes = shape
+    rng = np.random.default_rng(sum(shape))
+    w = rng.integers(-127, 128, (e_out, e_in))
+    if e_in * 127 * 255 >= 2 ** 31 or float(np.abs(w).max()) * e_in * (1 << 18) >= 2 ** 53:
+        w = rng.integers(-1, 2, (e_out, e_in))
+    rows = u53(sum(shape) + 1, (e_in, lanes))
+    ps = lin._dense_pass(w)
+    _, mt = lin.split_mma_tiles(ps)
+    assert mt is not None
+    got = lin.int_matmul_mod_q(w, rows)
+    assert np.array_equal(got, olo.int_matmul_exact_objects(w, rows))
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("r", [0, 1, 2, 7, 13, 19])
+def test_mma_round_matches_cuda_core_kernel(r, monkeypatch):
+    """A full ResNet-20 round map (maps, residual extras, bias) through both kernels."""
+    import torch
+    from paper_2509_01253_b200.device import RingContext
+    from paper_2509_01253_b200.params import preset_for_bits
+    model = W.resnet20_model(12, 0)
+    sch = preset_for_bits(12, 0)
+    R = sch.ring
+    ctx = RingContext.get(R.t, R.alpha, R.p_bits, sch.gadget.D, sch.gadget.l, 0, sch.beta, 0)
+    rnd = model.rounds[r]
+    E = rnd.input_len
+    rng = np.random.default_rng(r)
+    x = torch.from_numpy(rng.integers(0, 1 << 53, (E, 2, R.N), dtype=np.uint64).view(np.int64)).cuda()
+    in_map = torch.from_numpy(rng.permutation(E).astype(np.int64)).cuda()
+    out_map = torch.from_numpy(rng.permutation(rnd.output_len).astype(np.int64)).cuda()
+    unit = torch.from_numpy(rng.integers(0, 1 << 53, R.N, dtype=np.uint64).view(np.int64)).cuda()
+    passes = mm.lower_round(model, r)
+    if r == 1:  # exercise the bias path as well
+        passes[-1].bias = rng.integers(-5, 6, passes[-1].out_len)
+    outs = []
+    for enabled in (True, False):
+        monkeypatch.setattr(lin, "MMA_ENABLED", enabled)
+        dps = [lin.DevicePass(p, ctx.dev) for p in passes]
+        assert (dps[0].n_mma_tiles > 0) == enabled or r == 19
+        out = torch.zeros((rnd.output_len, 2, R.N), dtype=torch.int64, device=ctx.dev)
+        lin.run_round(ctx, dps, x, in_map, out, out_map, unit)
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
