@@ -118,11 +118,12 @@ typedef struct {
   int64_t lanes;             /* u64 lanes per row; 0 = 2N (ciphertext rows) */
   int64_t body_off;          /* first lane receiving bias*unit (N for ciphertext rows) */
   /* Optional tensor-core tile groups (tcgen05 kind::i8; |w| <= 127): output
-   * rows of consecutive shared-column groups merged into tiles of <= 256 rows.
-   * The groups above must then exclude those rows. */
+   * rows of consecutive shared-column groups merged into tiles of <= 256 rows,
+   * their residual extras folded in as taps (the CSR extras above then apply
+   * only to the groups, which must exclude the tile rows). */
   const int32_t* mma_tiles;  /* (n_mma_tiles, 8): cols_off, K_pad, w_off, rows_off, nrows, N_pad, 0, 0 */
   int64_t n_mma_tiles;
-  const int32_t* mma_cols;   /* K_pad input-column indices per tile (-1 = zero tap) */
+  const int32_t* mma_cols;   /* K_pad taps per tile: >= 0 pass-input row, -1 zero, <= -2 round-input row -(v+2) */
   const int32_t* mma_rows;   /* canonical output row of each tile row */
   const uint8_t* mma_w;      /* packed s8 weights, UMMA K-major no-swizzle core matrices */
   int32_t mma_max_np, mma_max_kp;  /* largest N_pad / K_pad over the tiles */

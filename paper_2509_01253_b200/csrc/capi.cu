@@ -417,9 +417,6 @@ int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* d, void* stream) {
     m.tcols = d->mma_cols;
     m.trows = d->mma_rows;
     m.tw = d->mma_w;
-    m.ex_ptr = a.ex_ptr;
-    m.ex_col = a.ex_col;
-    m.ex_w = a.ex_w;
     m.bias = a.bias;
     m.unit = a.unit;
     m.T = d->n_mma_tiles;

@@ -13,14 +13,16 @@
 // is the exact reference result.  Byte 7 of a lane is always 0 (values
 // < 2^53), so 7/8 of the tensor work is useful.
 //
-// Per CTA: one tile group (<= 256 output rows sharing one column list) over a
-// contiguous range of 128-byte M-tiles.  Pipeline: all 128 threads gather the
-// K taps of the next stages with cp.async (16 B, zero-fill for padding taps
-// and row tails) straight into the 128B-swizzled canonical layout; one thread
+// Per CTA: one tile group (<= 256 output rows sharing one column list; the
+// residual skip rows are folded in as extra taps with identity weights) over a
+// contiguous range of 128-byte M-tiles.  Warp-specialised pipeline: 4 producer
+// warps gather the K taps of each stage with cp.async (16 B, zero-fill for
+// padding taps and row tails) straight into the 128B-swizzled canonical layout
+// and arrive on the stage's mbarrier when their copies land; one MMA warp
 // issues the MMAs (K = 32 each) into a double-buffered TMEM accumulator and
-// commits to per-stage mbarriers; the epilogue of tile t-1 (tcgen05.ld ->
-// smem transpose -> byte recombination, residual extras, bias*unit, sigma_r
-// scatter) runs while tile t's MMAs are in flight.
+// commits to per-stage / per-accumulator mbarriers; 4 epilogue warps
+// (tcgen05.ld -> per-warp smem transpose -> byte recombination, bias*unit,
+// sigma_r scatter) drain tile t-1 while tile t is being gathered and multiplied.
 #include "sfhr_common.cuh"
 #include "sfhr_kernels.h"
 
@@ -28,7 +30,9 @@ namespace sfhr {
 
 namespace {
 
-constexpr int MMA_THREADS = 128;
+constexpr int EPI_WARPS = 4;              // TMEM lanes 0-127
+constexpr int PRODUCERS = 128;            // cp.async gather threads
+constexpr int MMA_THREADS = EPI_WARPS * 32 + PRODUCERS + 32;
 constexpr int KC = 64;                    // taps per pipeline stage (2 MMAs)
 constexpr int NSTAGE = 4;
 constexpr int STAGE_BYTES = KC * 128;     // 8 KB
@@ -115,19 +119,21 @@ struct MmaSmem {
     s.ring = 0;
     s.b = s.ring + NSTAGE * STAGE_BYTES;
     s.ep = s.b + ((Np * Kp + 127) & ~127);
-    s.colp = s.ep + EP_COLS * 128 * 4;
+    s.colp = s.ep + EPI_WARPS * EP_COLS * 32 * 4;
     s.odst = s.colp + Kp * 8;
     s.ocan = s.odst + Np * 8;
     s.bars = (s.ocan + Np * 4 + 7) & ~7;
-    s.tslot = s.bars + (NSTAGE + 2) * 8;
+    s.tslot = s.bars + (2 * NSTAGE + 4) * 8;
     s.total = s.tslot + 16 + 1024;  // + alignment slack for the 1024-B swizzle atoms
     return s;
   }
 };
 
+// Warp roles: 0-3 epilogue (TMEM lanes 32w..32w+31), 4-7 producers (cp.async
+// gathers, one mbarrier arrival per thread per stage), 8 MMA issuer.
 __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_constant__ LinearMmaArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tg = (int)(blockIdx.x % a.T);
   const int chunk = (int)(blockIdx.x / a.T);
   const int32_t* td = a.tiles + 8 * (int64_t)tg;
@@ -143,21 +149,32 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   unsigned char* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   const MmaSmem L = MmaSmem::make(Np, Kp);
   const uint32_t ring = su32(sm + L.ring), bsm = su32(sm + L.b);
-  int32_t* ep = reinterpret_cast<int32_t*>(sm + L.ep);
-  int64_t* colp = reinterpret_cast<int64_t*>(sm + L.colp);
+  const unsigned char** colp = reinterpret_cast<const unsigned char**>(sm + L.colp);
   int64_t* odst = reinterpret_cast<int64_t*>(sm + L.odst);
   int32_t* ocan = reinterpret_cast<int32_t*>(sm + L.ocan);
-  const uint32_t bars = su32(sm + L.bars);  // [0, NSTAGE): stage free; NSTAGE + {0,1}: accumulator ready
+  // barriers: full[NSTAGE] (128 producer arrivals), empty[NSTAGE] (MMA commit),
+  // acc_full[2] (MMA commit), acc_empty[2] (4 epilogue warps)
+  const uint32_t bars = su32(sm + L.bars);
+  const uint32_t full0 = bars, empty0 = bars + 8 * NSTAGE, accf0 = bars + 16 * NSTAGE, acce0 = accf0 + 16;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + L.tslot);
   const uint32_t ncols = 2 * Np <= 32 ? 32 : 2 * Np <= 64 ? 64 : 2 * Np <= 128 ? 128 : 2 * Np <= 256 ? 256 : 512;
 
-  // ---- setup: B operand (weights), tap offsets, output row maps, barriers, TMEM ----
+  // ---- setup: B operand (weights), tap row pointers, output row maps, barriers, TMEM ----
   const unsigned char* wsrc = a.tw + w0;
   for (int i = tid; i < Np * Kp / 16; i += MMA_THREADS) cp16(bsm + 16 * i, wsrc + 16 * i, 16);
   cp_commit();
+  const unsigned char* in8 = reinterpret_cast<const unsigned char*>(a.in);
+  const unsigned char* rin8 = reinterpret_cast<const unsigned char*>(a.round_in);
   for (int k = tid; k < Kp; k += MMA_THREADS) {
     const int col = a.tcols[c0 + k];
-    colp[k] = col < 0 ? -1 : (a.in_map ? a.in_map[col] : (int64_t)col) * rowbytes;
+    const unsigned char* p = nullptr;
+    if (col >= 0) {
+      p = in8 + (a.in_map ? a.in_map[col] : (int64_t)col) * rowbytes;
+    } else if (col <= -2) {  // folded residual extra: a row of the ROUND input
+      const int rc = -(col + 2);
+      p = rin8 + (a.round_map ? a.round_map[rc] : (int64_t)rc) * rowbytes;
+    }
+    colp[k] = p;
   }
   for (int o = tid; o < Np; o += MMA_THREADS) {
     if (o < nr) {
@@ -170,7 +187,14 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
     }
   }
   if (tid == 0) {
-    for (int i = 0; i < NSTAGE + 2; ++i) mbar_init(bars + 8 * i, 1);
+    for (int i = 0; i < NSTAGE; ++i) {
+      mbar_init(full0 + 8 * i, PRODUCERS);
+      mbar_init(empty0 + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(accf0 + 8 * i, 1);
+      mbar_init(acce0 + 8 * i, EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
@@ -185,103 +209,109 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-
-  // kind::i8, D = s32, A = u8 (MN-major), B = s8 (K-major), M = 128, N = Np
-  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(Np >> 3) << 17) |
-                         ((128u >> 4) << 24);
   const int nkc = (Kp + KC - 1) / KC;
-  const int total = (mt1 - mt0) * nkc;
-  const uint32_t b_kblock = (uint32_t)(Np / 8) * 128;  // bytes per 16-byte K block of B
 
-  auto issue = [&](int it) {
-    const int mt = mt0 + it / nkc, kc = it - (it / nkc) * nkc;
-    const uint32_t dst0 = ring + (it % NSTAGE) * STAGE_BYTES;
-    const int ntaps = min(KC, Kp - kc * KC);
-    const int64_t boff = (int64_t)mt * 128;
-    for (int q = tid; q < ntaps * 8; q += MMA_THREADS) {
-      const int tap = q >> 3, c = q & 7;
-      const int64_t cpos = colp[kc * KC + tap];
-      const int64_t off = boff + c * 16;
-      const bool ok = cpos >= 0 && off < rowbytes;
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(a.in) + (ok ? cpos + off : 0);
-      cp16(dst0 + tap * 128 + ((c ^ (tap & 7)) << 4), src, ok ? 16u : 0u);
-    }
-  };
-
-  auto epilogue = [&](int mtl) {
-    const int buf = mtl & 1;
-    mbar_wait(bars + 8 * (NSTAGE + buf), (uint32_t)((mtl >> 1) & 1));
-    tc_fence_after();
-    const int64_t lane0 = (int64_t)(mt0 + mtl) * 16;
-    for (int cc = 0; cc < Np; cc += EP_COLS) {
-      uint32_t r[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * Np + cc), r);
+  if (warp >= EPI_WARPS && warp < EPI_WARPS + PRODUCERS / 32) {
+    // ---------------- producers ----------------
+    const int pt = tid - EPI_WARPS * 32;
+    const int c = pt & 7, tb = pt >> 3;          // 16-byte chunk, first tap (taps tb + 16 i)
+    const uint32_t dst_lane = (uint32_t)(tb * 128 + ((c ^ (tb & 7)) << 4));
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int mt = mt0; mt < mt1; ++mt) {
+      const int64_t off = (int64_t)mt * 128 + c * 16;
+      const uint32_t nbytes = off < rowbytes ? 16u : 0u;
+      for (int kc = 0; kc < nkc; ++kc) {
+        mbar_wait(empty0 + 8 * stage, phase ^ 1);
+        const int ntaps = min(KC, Kp - kc * KC);
+        const unsigned char* const* cp = colp + kc * KC;
+        const uint32_t dst = ring + stage * STAGE_BYTES + dst_lane;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) ep[j * 128 + tid] = (int32_t)r[j];
-      __syncthreads();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int idx = tid + MMA_THREADS * h;
-        const int c = idx >> 4, u = idx & 15;
-        const int o = cc + c;
-        const int64_t ln = lane0 + u;
-        if (o < nr && ln < lanes) {
-          const int4* p = reinterpret_cast<const int4*>(ep + c * 128 + u * 8);
-          const int4 x0 = p[0], x1 = p[1];
-          uint64_t v = sx(x0.x) + (sx(x0.y) << 8) + (sx(x0.z) << 16) + (sx(x0.w) << 24) +
-                       (sx(x1.x) << 32) + (sx(x1.y) << 40) + (sx(x1.z) << 48) + (sx(x1.w) << 56);
-          const int oc = ocan[o];
-          if (a.ex_ptr) {
-            const int e0 = a.ex_ptr[oc], e1 = a.ex_ptr[oc + 1];
-            for (int e = e0; e < e1; ++e) {
-              const int col = a.ex_col[e];
-              const int64_t src = a.round_map ? a.round_map[col] : (int64_t)col;
-              v += sx(a.ex_w[e]) * (uint64_t)a.round_in[src * lanes + ln];
-            }
+        for (int i = 0; i < KC / 16; ++i) {
+          const int tap = tb + 16 * i;
+          if (tap < ntaps) {
+            const unsigned char* rp = cp[tap];
+            cp16(dst + i * 16 * 128, rp ? rp + off : in8, rp ? nbytes : 0u);
           }
-          if (a.bias && ln >= a.body_off) v += (uint64_t)a.bias[oc] * a.unit[ln - a.body_off];
-          a.out[odst[o] * lanes + ln] = v & QMASK;
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(full0 + 8 * stage)
+                     : "memory");
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
         }
       }
-      __syncthreads();
     }
-    tc_fence_before();
-  };
-
-  // ---- main pipeline ----
-  for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < total) issue(s);
-    cp_commit();
-  }
-  for (int it = 0; it < total; ++it) {
-    const int nx = it + NSTAGE - 1;
-    if (nx < total) {
-      if (it >= 1) mbar_wait(bars + 8 * ((it - 1) % NSTAGE), (uint32_t)(((it - 1) / NSTAGE) & 1));
-      issue(nx);
-    }
-    cp_commit();
-    cp_wait<NSTAGE - 1>();
-    fence_proxy_async();
-    __syncthreads();
-    const int mtl = it / nkc, kc = it - mtl * nkc, s = it % NSTAGE;
-    const int buf = mtl & 1;
-    if (tid == 0) {
+  } else if (warp == EPI_WARPS + PRODUCERS / 32) {
+    // ---------------- MMA issuer ----------------
+    // kind::i8, D = s32, A = u8 (MN-major), B = s8 (K-major), M = 128, N = Np
+    const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(Np >> 3) << 17) |
+                           ((128u >> 4) << 24);
+    const uint32_t b_kblock = (uint32_t)(Np / 8) * 128;  // bytes per 16-byte K block of B
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int mtl = 0; mtl < mt1 - mt0; ++mtl) {
+      const int buf = mtl & 1;
+      mbar_wait(acce0 + 8 * buf, (uint32_t)(((mtl >> 1) & 1) ^ 1));
       tc_fence_after();
-      const int nmma = min(KC, Kp - kc * KC) / 32;
-      for (int j = 0; j < nmma; ++j) {
-        const uint64_t ad = sdesc(ring + s * STAGE_BYTES + j * 4096, 16, 1024, 2);
-        const int kb = (kc * KC + j * 32) >> 4;
-        const uint64_t bd = sdesc(bsm + kb * b_kblock, b_kblock, 128, 0);
-        mma_i8(tmem + (uint32_t)(buf * Np), ad, bd, idesc, (kc > 0 || j > 0) ? 1u : 0u);
+      for (int kc = 0; kc < nkc; ++kc) {
+        mbar_wait(full0 + 8 * stage, phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const int nmma = min(KC, Kp - kc * KC) / 32;
+          for (int j = 0; j < nmma; ++j) {
+            const uint64_t ad = sdesc(ring + stage * STAGE_BYTES + j * 4096, 16, 1024, 2);
+            const int kb = (kc * KC + j * 32) >> 4;
+            const uint64_t bd = sdesc(bsm + kb * b_kblock, b_kblock, 128, 0);
+            mma_i8(tmem + (uint32_t)(buf * Np), ad, bd, idesc, (kc > 0 || j > 0) ? 1u : 0u);
+          }
+          mma_commit(empty0 + 8 * stage);
+          if (kc == nkc - 1) mma_commit(accf0 + 8 * buf);
+        }
+        __syncwarp();
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
-      mma_commit(bars + 8 * s);
-      if (kc == nkc - 1) mma_commit(bars + 8 * (NSTAGE + buf));
     }
-    __syncwarp();
-    if (kc == nkc - 1 && mtl > 0) epilogue(mtl - 1);
+  } else if (warp < EPI_WARPS) {
+    // ---------------- epilogue ----------------
+    int32_t* ep = reinterpret_cast<int32_t*>(sm + L.ep) + warp * (EP_COLS * 32);
+    for (int mtl = 0; mtl < mt1 - mt0; ++mtl) {
+      const int buf = mtl & 1;
+      mbar_wait(accf0 + 8 * buf, (uint32_t)((mtl >> 1) & 1));
+      tc_fence_after();
+      const int64_t lane0 = (int64_t)(mt0 + mtl) * 16 + warp * 4;  // this warp's 4 u64 lanes
+      for (int cc = 0; cc < Np; cc += EP_COLS) {
+        uint32_t r[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * Np + cc), r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) ep[j * 32 + lane] = (int32_t)r[j];
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int idx = lane + 32 * h;
+          const int cl = idx >> 2, u = idx & 3;
+          const int o = cc + cl;
+          const int64_t ln = lane0 + u;
+          if (o < nr && ln < lanes) {
+            const int4* p = reinterpret_cast<const int4*>(ep + cl * 32 + u * 8);
+            const int4 x0 = p[0], x1 = p[1];
+            uint64_t v = sx(x0.x) + (sx(x0.y) << 8) + (sx(x0.z) << 16) + (sx(x0.w) << 24) +
+                         (sx(x1.x) << 32) + (sx(x1.y) << 40) + (sx(x1.z) << 48) + (sx(x1.w) << 56);
+            if (a.bias && ln >= a.body_off) v += (uint64_t)a.bias[ocan[o]] * a.unit[ln - a.body_off];
+            a.out[odst[o] * lanes + ln] = v & QMASK;
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(acce0 + 8 * buf) : "memory");
+    }
   }
-  epilogue(mt1 - mt0 - 1);
 
+  tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 0)

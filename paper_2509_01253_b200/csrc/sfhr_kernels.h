@@ -85,12 +85,9 @@ struct LinearMmaArgs {
   uint64_t* out;
   const int64_t* out_map;
   const int32_t* tiles;      // (T, 8): cols_off, K_pad, w_off (bytes), rows_off, nrows, N_pad, 0, 0
-  const int32_t* tcols;      // K_pad column indices per tile (-1 = zero tap)
+  const int32_t* tcols;      // K_pad taps per tile: >= 0 pass-input row, -1 zero, <= -2 round-input row -(v+2)
   const int32_t* trows;      // canonical output rows per tile
   const uint8_t* tw;         // packed s8 B operands (UMMA K-major, no swizzle)
-  const int32_t* ex_ptr;
-  const int32_t* ex_col;
-  const int32_t* ex_w;
   const int64_t* bias;
   const uint64_t* unit;
   int64_t T;

@@ -84,29 +84,52 @@ def split_mma_tiles(ps: LinearPass):
             run.append(j)
             tot += nrj
             j += 1
-        k_pad = (nc + 31) // 32 * 32
+        rows_run = np.concatenate([ps.rows[int(g[q][3]):int(g[q][3]) + int(g[q][4])] for q in run])
+        # residual extras (CSR into the round input) become extra taps
+        ex_cols, ex_vals = np.zeros(0, np.int64), None
+        if ps.ex_ptr is not None:
+            lo, hi = ps.ex_ptr[rows_run], ps.ex_ptr[rows_run + 1]
+            if np.any(hi > lo):
+                idx = np.concatenate([np.arange(a, b) for a, b in zip(lo, hi)])
+                ex_cols = np.unique(ps.ex_col[idx])
+                ex_vals = np.zeros((tot, len(ex_cols)), np.int64)
+                for ri, (a, b) in enumerate(zip(lo, hi)):
+                    np.add.at(ex_vals[ri], np.searchsorted(ex_cols, ps.ex_col[a:b]), ps.ex_w[a:b])
+        kk = nc + len(ex_cols)
+        k_pad = (kk + 31) // 32 * 32
         n_pad = (tot + 15) // 16 * 16
         key = tuple(int(g[q][2]) for q in run) + tuple(int(g[q][4]) for q in run)
-        if key in cache:
+        if ex_vals is not None:
+            key = None
+        if key is not None and key in cache:
             woff = cache[key]
         else:
             wt = np.concatenate([wv[int(g[q][2]):int(g[q][2]) + nc * ROWS_PER_GROUP]
                                  .reshape(nc, ROWS_PER_GROUP)[:, :int(g[q][4])].T for q in run])
-            if np.abs(wt).max(initial=0) > 127 or n_pad * k_pad > MMA_MAX_BYTES:
+            if ex_vals is not None:
+                wt = np.concatenate([wt, ex_vals], axis=1)
+            if np.abs(wt).max(initial=0) > 127 or n_pad * k_pad > MMA_MAX_BYTES or len(ex_cols) > 256:
                 rest.extend(run)
                 i = j
                 continue
-            woff = nw
-            packed = _pack_umma_k_major(wt.astype(np.int8), n_pad, k_pad)
-            tw.append(packed)
-            nw += packed.size
-            cache[key] = woff
+            if key is None:  # identical extras structure repeats per pixel: cache on the weights
+                key = ("w", wt.tobytes(), n_pad, k_pad)
+                woff = cache.get(key)
+            else:
+                woff = None
+            if woff is None:
+                woff = nw
+                packed = _pack_umma_k_major(wt.astype(np.int8), n_pad, k_pad)
+                tw.append(packed)
+                nw += packed.size
+                cache[key] = woff
         tiles.append((ncols, k_pad, woff, nrows, tot, n_pad, 0, 0))
         tc = np.full(k_pad, -1, np.int64)
         tc[:nc] = cols
+        tc[nc:kk] = -(ex_cols + 2)
         tcols.append(tc)
         ncols += k_pad
-        trows.append(np.concatenate([ps.rows[int(g[q][3]):int(g[q][3]) + int(g[q][4])] for q in run]))
+        trows.append(rows_run)
         nrows += tot
         max_np, max_kp = max(max_np, n_pad), max(max_kp, k_pad)
         i = j

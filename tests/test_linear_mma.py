@@ -21,13 +21,15 @@ def _unpack(tw, n_pad, k_pad):
     return tw.reshape(k_pad // 16, n_pad // 8, 8, 16).transpose(1, 2, 0, 3).reshape(n_pad, k_pad)
 
 
-def _emulate_tile(mt, t, rows_in):
+def _emulate_tile(mt, t, rows_in, round_in=None):
     """numpy replay of one tile group: byte-plane int8 GEMM + recombination."""
     c0, kp, w0, r0, nr, np_, _, _ = (int(x) for x in mt.tiles[t])
     B = _unpack(mt.w[w0:w0 + np_ * kp], np_, kp).astype(np.int64)      # (N_pad, K_pad) s8
     cols = mt.cols[c0:c0 + kp]
     X = np.zeros((kp,) + rows_in.shape[1:], np.uint64)
     X[cols >= 0] = rows_in[cols[cols >= 0]]
+    if np.any(cols <= -2):  # folded residual extras read the round input
+        X[cols <= -2] = round_in[-(cols[cols <= -2] + 2)]
     Xb = X.reshape(kp, -1).view(np.uint8).reshape(kp, -1, 8).astype(np.int64)  # (K, lanes, 8 bytes)
     D = np.einsum("ok,klj->olj", B[:nr], Xb)                            # s32-exact accumulators
     assert np.abs(D).max(initial=0) < 2 ** 31
@@ -39,6 +41,7 @@ def _emulate_tile(mt, t, rows_in):
 
 PASSES = {
     "resnet20_r1": lambda: mm.lower_round(W.resnet20_model(12, 0), 1),
+    "resnet20_r2_residual": lambda: mm.lower_round(W.resnet20_model(12, 0), 2),
     "resnet20_r7": lambda: mm.lower_round(W.resnet20_model(12, 0), 7),
     "resnet20_fc": lambda: mm.lower_round(W.resnet20_model(12, 0), 19),
     "toy": lambda: mm.lower_round(W.toy_model(8, 3), 0),
@@ -78,9 +81,20 @@ def test_tiles_cover_rows_once_and_replay_exactly(name):
                     if col >= 0:
                         Wd[ps.rows[r0 + i], col] += blk[c, i]
         x = rng.integers(0, 1 << 53, (ps.in_len, 2, 5), dtype=np.uint64)
+        xr, We = None, None
+        if ps.ex_ptr is not None:
+            xr = rng.integers(0, 1 << 53, (int(ps.ex_col.max()) + 1, 2, 5), dtype=np.uint64)
+            We = np.zeros((ps.out_len, len(xr)), np.int64)
+            for o in range(ps.out_len):
+                for e in range(ps.ex_ptr[o], ps.ex_ptr[o + 1]):
+                    We[o, ps.ex_col[e]] += ps.ex_w[e]
         for t in sorted({0, len(mt.tiles) // 2, len(mt.tiles) - 1}):
-            rows, got = _emulate_tile(mt, t, x)
-            want = olo.int_matmul_exact_objects(Wd[rows], x).reshape(len(rows), -1)
+            rows, got = _emulate_tile(mt, t, x, xr)
+            if We is None:
+                want = olo.int_matmul_exact_objects(Wd[rows], x).reshape(len(rows), -1)
+            else:
+                want = olo.int_matmul_exact_objects(np.concatenate([Wd[rows], We[rows]], 1),
+                                                    np.concatenate([x, xr])).reshape(len(rows), -1)
             assert np.array_equal(got, want), (name, t)
 
 
