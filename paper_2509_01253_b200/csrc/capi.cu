@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -50,6 +51,7 @@ struct sfhr_key {
 namespace {
 thread_local std::string g_err;
 std::atomic<unsigned long long> g_launches{0};  // kernels launched through this library
+const bool g_debug_sync = std::getenv("SFHR_DEBUG_SYNC") != nullptr;
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -130,6 +132,14 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     return SFHR_OK;
   }
   CK(launch_stage(P.rc, a, st), "stage kernel");
+  if (g_debug_sync) {  // SFHR_DEBUG_SYNC=1: locate a faulting launch
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      std::fprintf(stderr, "[sfhr] stage kernel failed: B=%lld nreps=%d identity=%d in=%p out=%p: %s\n",
+                   (long long)B, a.nreps, identity, (const void*)in, (void*)out, cudaGetErrorString(e));
+      return cuda_fail(e, "stage kernel (debug sync)");
+    }
+  }
   ++g_launches;
   if (e0) {
     CK(cudaEventRecord(e1, st), "event record");

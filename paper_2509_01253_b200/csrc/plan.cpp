@@ -232,6 +232,21 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
         pc.z[k][m] = mont(powmod(zeta, (uint64_t)((k * m) % t), p));
         pc.zi[k][m] = mont(powmod(zeta, (uint64_t)((t - (k * m) % t) % t), p));
       }
+    // symmetric-pair DFT constants (keyswitch.cu dft_sym): a_m = x_m + x_{t-m} < 4p and
+    // sum_m a_m c_km over (t-1)/2 terms must stay below p 2^32; y_0 < 2tp below 2^32
+    {
+      const int H = (t - 1) / 2;
+      if (4.0L * H * (long double)p >= 4294967296.0L || 2.0L * t * (long double)p >= 4294967296.0L)
+        throw std::invalid_argument("NTT prime too large for the symmetric DFT ranges");
+      const uint64_t inv2 = (p + 1) / 2;
+      for (int k = 1; k <= H; ++k)
+        for (int m = 1; m <= H; ++m) {
+          const uint64_t zp = powmod(zeta, (uint64_t)((k * m) % t), p);
+          const uint64_t zm = powmod(zeta, (uint64_t)((t - (k * m) % t) % t), p);
+          pc.hc[k - 1][m - 1] = mont(mulmod((zp + zm) % p, inv2, p));
+          pc.hs[k - 1][m - 1] = mont(mulmod((zp + p - zm) % p, inv2, p));
+        }
+    }
     // CRT: Q_i = P / p_i, Qinv = Q_i^-1 mod p_i
     uint64_t qmod64 = 1, qmodp = 1;
     for (int j = 0; j < rc.np; ++j)

@@ -30,6 +30,8 @@ struct PrimeConst {
   uint32_t z[MAXT][MAXT];   // zeta^(k m) * R mod p, zeta = omega^(M/t)
   uint32_t zi[MAXT][MAXT];  // zeta^(-k m) * R mod p
   uint32_t g[MAXT][MAXT];   // inverse first step [j][r-1]: (zeta^(-rj) - zeta^r) / M * Qinv * R
+  uint32_t hc[MAXT / 2][MAXT / 2];  // symmetric DFT: (zeta^(km) + zeta^(-km)) / 2 * R, k, m = 1..(t-1)/2
+  uint32_t hs[MAXT / 2][MAXT / 2];  //                (zeta^(km) - zeta^(-km)) / 2 * R
   uint64_t q_mod64;         // (P / p) mod 2^64
   double inv_p;             // 1.0 / p
 };

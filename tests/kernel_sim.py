@@ -3,7 +3,8 @@
 Replays, with the library's own constant tables (planning-only context, no
 GPU), exactly the arithmetic of ks_stage_kernel / ks_spectra_kernel in
 paper_2509_01253_b200/csrc/keyswitch.cu: Montgomery REDC with lazy [0, 2p)
-ranges, the fused automorphism+decomposition first step, radix-t DIF/DIT
+ranges, the symmetric-pair radix-t DFT (dft_sym, lazy [0, 6p) outputs before
+twiddles), the fused automorphism+decomposition first step, radix-t DIF/DIT
 stages, NTT-domain accumulation over reps, and explicit CRT mod 2^53.
 Every REDC input is range-checked, so an overflow in the kernel's bound
 reasoning fails here on CPU before any GPU time is spent.
@@ -54,6 +55,9 @@ class Prime:
         self.z = np.array([[pc.z[k][m] for m in range(T)] for k in range(T)], dtype=U)
         self.zi = np.array([[pc.zi[k][m] for m in range(T)] for k in range(T)], dtype=U)
         self.g = np.array([[pc.g[j][r] for r in range(T - 1)] for j in range(T - 1)], dtype=U)
+        H = (T - 1) // 2
+        self.hc = np.array([[pc.hc[k][m] for m in range(H)] for k in range(H)], dtype=U)
+        self.hs = np.array([[pc.hs[k][m] for m in range(H)] for k in range(H)], dtype=U)
         self.q_mod64 = U(pc.q_mod64)
         self.inv_p = pc.inv_p
         self.wt = sp.tw[i]
@@ -94,6 +98,43 @@ class Prime:
             out.append(self.redc(s))
         return out
 
+    def barrett(self, v):
+        v = np.asarray(v, dtype=U)
+        assert np.all(v < U(1 << 32))
+        r = v - ((v * self.mu) >> U(32)) * self.p
+        assert np.all(r < U(2) * self.p)
+        return r
+
+    def dft_sym(self, xs, inv=False, red=False):
+        """keyswitch.cu dft_sym: symmetric-pair radix-t DFT with its lazy ranges."""
+        T = len(xs)
+        H = (T - 1) // 2
+        p2 = U(2) * self.p
+        xs = [np.asarray(x, dtype=U) for x in xs]
+        for x in xs:
+            assert np.all(x < p2), "DFT input >= 2p"
+        a = [xs[m] + xs[T - m] for m in range(1, H + 1)]
+        b = [xs[m] + p2 - xs[T - m] for m in range(1, H + 1)]
+        y0 = xs[0] + sum(a)
+        out = [None] * T
+        out[0] = self.barrett(y0)
+        for k in range(1, H + 1):
+            sp = sum(a[m] * self.hc[k - 1][m] for m in range(H))
+            sq = sum(b[m] * self.hs[k - 1][m] for m in range(H))
+            P, Q = self.redc(sp), self.redc(sq)
+            u, v = xs[0] + P + Q, xs[0] + P + p2 - Q
+            assert np.all(u < U(1 << 32)) and np.all(v < U(1 << 32))
+            if red:
+                u, v = self.barrett(u), self.barrett(v)
+            out[k], out[T - k] = (v, u) if inv else (u, v)
+        return out
+
+    def mont6(self, a, bm):
+        """mont_mul with a lazy [0, 6p) operand (twiddle after a symmetric DFT)."""
+        a = np.asarray(a, dtype=U)
+        assert np.all(a < U(6) * self.p)
+        return self.redc(a * np.asarray(bm, dtype=U))
+
 
 def forward(sp: SimPlan, pr: Prime, vals):
     """vals: (N,) residues < 2p (coefficient domain) -> (nitems, T) last-stage outputs."""
@@ -101,11 +142,9 @@ def forward(sp: SimPlan, pr: Prime, vals):
     A = np.asarray(vals, dtype=U).reshape(T - 1, n1)
     m = np.arange(n1)
     buf = np.zeros((T - 1, n1), U)
+    ys = pr.dft_sym([A[j] for j in range(T - 1)] + [np.zeros(n1, U)])
     for q in range(1, T):
-        s = np.zeros(n1, U)
-        for j in range(T - 1):
-            s = s + A[j] * pr.z[q][j]
-        buf[q - 1] = pr.mont(pr.redc(s), pr.wt[q * m])
+        buf[q - 1] = pr.mont6(ys[q], pr.wt[q * m])
     buf = buf.reshape(-1)
     nsub = n1 // T
     L = nsub
@@ -115,22 +154,22 @@ def forward(sp: SimPlan, pr: Prime, vals):
         step = M // (T * L)
         j = np.arange(L)
         xs = [v[:, :, mm, :] for mm in range(T)]
-        ys = pr.dft(xs, pr.z)
+        ys = pr.dft_sym(xs)
         nv = np.empty_like(v)
         nv[:, :, 0, :] = ys[0]
         for k in range(1, T):
-            nv[:, :, k, :] = pr.mont(ys[k], pr.wt[step * j * k][None, None, :])
+            nv[:, :, k, :] = pr.mont6(ys[k], pr.wt[step * j * k][None, None, :])
         buf = nv.reshape(-1)
         L //= T
     x = buf.reshape(sp.nitems, T)
-    ys = pr.dft([x[:, mm] for mm in range(T)], pr.z)
+    ys = pr.dft_sym([x[:, mm] for mm in range(T)], red=True)
     return np.stack(ys, axis=1)  # (nitems, T)
 
 
 def inverse(sp: SimPlan, pr: Prime, y):
     """y: (nitems, T) in [0,2p) -> (N,) CRT-weighted residues y_i in [0, p)."""
     T, n1, M = sp.t, sp.n1, sp.M
-    xs = pr.dft([y[:, k] for k in range(T)], pr.zi)
+    xs = pr.dft_sym([y[:, k] for k in range(T)], inv=True, red=True)
     buf = np.stack(xs, axis=1).reshape(-1)
     L = T
     for s_ in range(sp.alpha - 3, -1, -1):
@@ -140,7 +179,7 @@ def inverse(sp: SimPlan, pr: Prime, y):
         j = np.arange(L)
         zs = [v[:, :, 0, :]] + [pr.mont(v[:, :, k, :], pr.wt[M - step * j * k][None, None, :])
                                for k in range(1, T)]
-        xs = pr.dft(zs, pr.zi)
+        xs = pr.dft_sym(zs, inv=True, red=True)
         buf = np.stack(xs, axis=2).reshape(-1)
         L *= T
     v = buf.reshape(T - 1, n1)
