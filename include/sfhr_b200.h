@@ -55,7 +55,8 @@ int sfhr_ctx_destroy(sfhr_ctx* ctx);
 int sfhr_ctx_info(const sfhr_ctx* ctx, int64_t* info, int n);
 
 /* Debug/verification: copy the device constant block (RingConst, size
- * sfhr_ringconst_bytes()) and the [np][M+1] Montgomery twiddle table. */
+ * sfhr_ringconst_bytes()) and the [np][(M + 4) & ~3] Montgomery twiddle table
+ * (rows padded to a multiple of 4 words; entries 0..M used). */
 size_t sfhr_ringconst_bytes(void);
 int sfhr_ctx_debug_tables(const sfhr_ctx* ctx, void* ringconst, size_t rc_bytes, uint32_t* twid,
                           size_t twid_words);

@@ -36,7 +36,7 @@ struct sfhr_ctx {
   bool prof = false;                 // time every stage launch with CUDA events
   std::vector<ProfRec> prof_recs;    // pending (unresolved) records
   std::vector<cudaEvent_t> ev_pool;  // recycled events
-  uint32_t* twid = nullptr;  // [np][M+1]
+  uint32_t* twid = nullptr;  // [np][twid_stride(M)]
   int32_t* cvec = nullptr;   // [N]
   std::mutex mu;
 };

@@ -293,7 +293,7 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst
   SmemLayout s;
   s.xa = reinterpret_cast<uint64_t*>(smem);
   s.wt = reinterpret_cast<uint32_t*>(smem + (size_t)rc.N * 8);
-  s.acc = s.wt + ((rc.M + 1 + 3) & ~3);
+  s.acc = s.wt + twid_stride(rc.M);
   s.buf = s.acc + 2 * rc.N;
   return s;
 }
@@ -310,16 +310,28 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   uint64_t* xout = a.out + row * 2 * (int64_t)N;
   cg::cluster_group cluster = cg::this_cluster();
 
-  // stage x.a and the twiddle table; detect an all-zero row
+  // stage x.a (16-byte loads) and the twiddle table; detect an all-zero row
+  // (the body is only read when the mask is all zero, which is rare)
   int nz = 0;
-  for (int k = threadIdx.x; k < N; k += blockDim.x) {
-    const uint64_t va = xin[k], vb = xin[N + k];
-    S.xa[k] = va;
-    nz |= (va | vb) != 0;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(xin);  // rows are 16-byte aligned (N even)
+    uint4* dst = reinterpret_cast<uint4*>(S.xa);
+    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {
+      const uint4 v = src[c];
+      dst[c] = v;
+      nz |= (v.x | v.y | v.z | v.w) != 0;
+    }
   }
-  const uint32_t* wsrc = a.twid + (size_t)PR * (M + 1);
-  for (int k = threadIdx.x; k <= M; k += blockDim.x) S.wt[k] = wsrc[k];
-  const int live = __syncthreads_or(nz);
+  {
+    const uint4* wsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)PR * twid_stride(M));
+    uint4* wdst = reinterpret_cast<uint4*>(S.wt);
+    for (int k = threadIdx.x; k < twid_stride(M) / 4; k += blockDim.x) wdst[k] = wsrc[k];
+  }
+  int live = __syncthreads_or(nz);
+  if (!live) {
+    for (int k = threadIdx.x; k < N; k += blockDim.x) nz |= xin[N + k] != 0;
+    live = __syncthreads_or(nz);
+  }
   const int per = (N + rc.np - 1) / rc.np;
   const int k0 = PR * per, k1 = min(N, k0 + per);
   if (!live) {
@@ -459,6 +471,23 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   inv_mid_stages<T, A, PR>(S.buf, 2, rc, S.wt);
   inv_first_step<T, A, PR>(S.buf, 2, rc, S.wt);
 
+  // ---- body term sum_r aut_r(x.b) of this CTA's slice, gathered from global into the
+  // (now free) accumulator region while the other CTAs of the cluster finish ----
+  uint64_t* bsum_s = reinterpret_cast<uint64_t*>(S.acc);  // (k1 - k0) u64 <= N u64
+  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    uint64_t bsum = a.identity ? xin[N + k] : 0ull;
+    const uint32_t kmod = (uint32_t)(k % n1);
+    for (int r = 0; r < a.nreps; ++r) {
+      const uint32_t dinv = a.dinv[r];
+      const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
+      const uint32_t s2 = fastmod((uint32_t)(N + kmod) * dinv, M, rc.magicM);
+      uint64_t v = s1 < (uint32_t)N ? xin[N + s1] : 0ull;
+      if (s2 < (uint32_t)N) v -= xin[N + s2];
+      bsum += v;
+    }
+    bsum_s[k - k0] = bsum;
+  }
+
   // ---- explicit CRT across the cluster through distributed shared memory ----
   cluster.sync();
   const uint32_t* ry[MAXNP];
@@ -480,18 +509,8 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
     }
     const uint64_t Av = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
     const uint64_t Bv = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
-    uint64_t bsum = a.identity ? xin[N + k] : 0ull;
-    const uint32_t kmod = (uint32_t)(k % n1);
-    for (int r = 0; r < a.nreps; ++r) {
-      const uint32_t dinv = a.dinv[r];
-      const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
-      const uint32_t s2 = fastmod((uint32_t)(N + kmod) * dinv, M, rc.magicM);
-      uint64_t v = s1 < (uint32_t)N ? xin[N + s1] : 0ull;
-      if (s2 < (uint32_t)N) v -= xin[N + s2];
-      bsum += v;
-    }
     xout[k] = ((a.identity ? S.xa[k] : 0ull) - Av) & QMASK;
-    xout[N + k] = (bsum - Bv) & QMASK;
+    xout[N + k] = (bsum_s[k - k0] - Bv) & QMASK;
   }
   cluster.sync();
 }
@@ -529,7 +548,7 @@ __device__ void spectra_body(const RingConst& rc, const SpecArgs a, unsigned cha
   const int N = rc.N;
   SmemLayout S = carve(smem, rc);
   const uint64_t* src = a.keys + (size_t)job * N;  // job = (slot*l + i)*2 + c
-  for (int k = threadIdx.x; k <= rc.M; k += blockDim.x) S.wt[k] = a.twid[(size_t)PR * (rc.M + 1) + k];
+  for (int k = threadIdx.x; k <= rc.M; k += blockDim.x) S.wt[k] = a.twid[(size_t)PR * twid_stride(rc.M) + k];
   for (int k = threadIdx.x; k < N; k += blockDim.x) {
     const uint64_t v = src[k] & QMASK;
     long long c = (long long)v;
@@ -572,7 +591,7 @@ __global__ void __launch_bounds__(512) ks_spectra_kernel(const __grid_constant__
 #if !defined(SFHR_KS_T)
 size_t stage_smem_bytes(const RingConst& rc) {
   const int nb = rc.l > 2 ? rc.l : 2;
-  return (size_t)rc.N * 8 + (size_t)((rc.M + 1 + 3) & ~3) * 4 + (size_t)(2 + nb) * rc.N * 4;
+  return (size_t)rc.N * 8 + (size_t)twid_stride(rc.M) * 4 + (size_t)(2 + nb) * rc.N * 4;
 }
 
 int stage_threads(const RingConst& rc) {

@@ -206,7 +206,7 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
   uint64_t Pmod = 1;
   for (uint64_t p : primes) Pmod *= p;
   rc.P_mod64 = Pmod;
-  P.twid.assign((size_t)rc.np * (M + 1), 0);
+  P.twid.assign((size_t)rc.np * twid_stride(M), 0);
   const uint64_t R32 = 1ull << 32;
   for (int i = 0; i < rc.np; ++i) {
     const uint64_t p = primes[i];
@@ -268,7 +268,7 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
       }
     uint64_t w = 1;
     for (long long e = 0; e <= M; ++e) {
-      P.twid[(size_t)i * (M + 1) + e] = mont(e == M ? 1 : w);
+      P.twid[(size_t)i * twid_stride(M) + e] = mont(e == M ? 1 : w);
       w = mulmod(w, omega, p);
     }
   }

@@ -48,6 +48,12 @@ struct RingConst {
   PrimeConst pc[MAXNP];
 };
 
+// row stride (u32 words) of the [np][M+1] twiddle table, padded for 16-byte loads
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline constexpr int twid_stride(int M) { return (M + 4) & ~3; }
+
 #ifdef __CUDACC__
 // x < p * 2^32  ->  x * 2^-32 mod p, in (0, 2p)
 __device__ __forceinline__ uint32_t redc(uint64_t x, uint32_t p, uint32_t pinv) {

@@ -18,7 +18,7 @@ struct StageArgs {
   int shrink;             // reduce 64-bit accumulators after every rep
   uint32_t dinv[MAXREPS]; // d^-1 mod M of each rep's automorphism (1 = none)
   const uint32_t* spec[MAXREPS];  // key spectra of each rep: [l][2][np][N]
-  const uint32_t* twid;   // [np][M+1] omega^e * R mod p
+  const uint32_t* twid;   // [np][twid_stride(M)] omega^e * R mod p (e <= M)
   unsigned long long* counter;    // live-row switch counter (may be null)
 };
 

@@ -34,10 +34,11 @@ class SimPlan:
         k = nat.lib.sfhr_ctx_info(h, info, 32)
         self.info = list(info[:k])
         np_ = self.info[3]
-        tw = np.zeros(np_ * (self.M + 1), np.uint32)
+        stride = (self.M + 4) & ~3  # csrc/sfhr_common.cuh twid_stride
+        tw = np.zeros(np_ * stride, np.uint32)
         nat.check(nat.lib.sfhr_ctx_debug_tables(h, C.byref(rc), C.sizeof(rc), tw.ctypes.data, tw.size))
         self.rc = rc
-        self.tw = tw.reshape(np_, self.M + 1).astype(U)
+        self.tw = tw.reshape(np_, stride)[:, :self.M + 1].astype(U)
         self.t, self.alpha, self.N, self.n1 = t, alpha, rc.N, rc.n1
         self.np, self.l = rc.np, rc.l
         self.nitems = rc.nitems
