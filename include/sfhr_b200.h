@@ -161,6 +161,22 @@ unsigned long long sfhr_launch_count(void);
 int sfhr_profile_enable(sfhr_ctx* ctx, int enable);
 int sfhr_profile_collect(sfhr_ctx* ctx, double* total_ms, long long* total_bytes, long long* launches);
 
+
+/* ---- standalone RNS negacyclic NTT (BASELINE configs[1]; no reference
+ * counterpart).  Residues are (batch, L, N) u64 on the
+ * DEVICE, each limb reduced mod its ~prime_bits-bit prime p = 1 (mod 2N).
+ * Forward: natural order in, bit-reversed out; inverse takes that order back
+ * and includes the N^-1 scaling.  In place. */
+typedef struct sfhr_ntt_plan sfhr_ntt_plan;
+int sfhr_ntt_plan_create(int log2n, int L, int prime_bits, int device, sfhr_ntt_plan** out);
+int sfhr_ntt_plan_destroy(sfhr_ntt_plan* plan);
+int sfhr_ntt_plan_primes(const sfhr_ntt_plan* plan, uint64_t* primes, int n);
+/* host copies of the [L][N] forward (psi^brv(k)) and inverse twiddles (inverse slot 0 = N^-1) */
+int sfhr_ntt_plan_tables(const sfhr_ntt_plan* plan, uint64_t* w, uint64_t* wi);
+int sfhr_ntt_forward(const sfhr_ntt_plan* plan, uint64_t* data, int64_t batch, void* stream);
+int sfhr_ntt_inverse(const sfhr_ntt_plan* plan, uint64_t* data, int64_t batch, void* stream);
+const char* sfhr_ntt_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif
