@@ -8,9 +8,11 @@
 // and bit-exactly against the plain-C oracle in oracle/ntt_ref.c.
 //
 // Algorithm: merged-twiddle Cooley-Tukey forward (natural order in,
-// bit-reversed out; twiddles psi^brv(k)) and Gentleman-Sande inverse, Harvey
-// lazy butterflies with Shoup multiplication (w' = floor(w 2^64 / p)), data in
-// [0, 4p) inside, fully reduced at the boundary.
+// bit-reversed out; twiddles psi^brv(k)) and Gentleman-Sande inverse with Shoup
+// multiplication (w' = floor(w 2^64 / p)).  Primes are < 2^50, so the 14 spare
+// bits of a u64 let the butterflies run without range corrections (forward:
+// values < (2 log2 N + 1) p; inverse: sums reduced once per radix-16 pass);
+// residues are fully reduced at the boundary.
 //
 // One HBM pass per transform: a polynomial is split over a thread-block
 // CLUSTER of C = max(1, N / 8192) CTAs, each holding a contiguous chunk of
@@ -39,6 +41,9 @@ namespace ntt {
 
 constexpr int CHUNK_MAX = 8192;  // residues per CTA
 constexpr int EPT = 16;          // residues per thread in a local pass
+#ifndef NTT_MINB
+#define NTT_MINB 2
+#endif
 
 struct Tables {
   const uint64_t* w;    // [L][N] psi^brv(k) (forward), k >= 1 used
@@ -46,6 +51,7 @@ struct Tables {
   const uint64_t* wi;   // [L][N] psi^-brv(k) (inverse); wi[0] = N^-1
   const uint64_t* wis;  // [L][N]
   const uint64_t* p;    // [L]
+  const uint64_t* mu;   // [L] floor(2^64 / p)
 };
 
 __device__ __forceinline__ uint64_t shoup(uint64_t x, uint64_t w, uint64_t ws, uint64_t p) {
@@ -53,13 +59,26 @@ __device__ __forceinline__ uint64_t shoup(uint64_t x, uint64_t w, uint64_t ws, u
   return x * w - q * p;  // in [0, 2p) for any x < 2^64
 }
 
-// forward CT butterfly, inputs/outputs in [0, 4p)
+// forward CT butterfly without range corrections: Shoup accepts any 64-bit Y and
+// returns t in [0, 2p), so an input bound X, Y < k p gives outputs < (k + 2) p.
+// After the 16 stages of N = 2^16 every value is < 33 p < 2^56 (p < 2^50 is
+// enforced by the planner), and one final reduction brings it to [0, p).
 __device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t p) {
-  const uint64_t p2 = 2 * p;
-  uint64_t x = X >= p2 ? X - p2 : X;
   const uint64_t t = shoup(Y, w, ws, p);
+  const uint64_t x = X;
   X = x + t;
-  Y = x - t + p2;
+  Y = x + (2 * p - t);
+}
+// inverse GS butterfly with lazy sums: X, Y < M (M a multiple of p) -> X' = X + Y < 2M,
+// Y' in [0, 2p); a local pass reduces once at its end
+__device__ __forceinline__ void gs_bfly_lazy(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t p,
+                                             uint64_t M) {
+  const uint64_t x = X, y = Y;
+  X = x + y;
+  Y = shoup(x + M - y, w, ws, p);
+}
+__device__ __forceinline__ uint64_t barrett2(uint64_t x, uint64_t p, uint64_t mu) {
+  return x - __umul64hi(x, mu) * p;  // x < 2^63 -> [0, 2p)
 }
 // inverse GS butterfly, inputs/outputs in [0, 2p)
 __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t p) {
@@ -72,44 +91,58 @@ __device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, ui
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }  // one pad word per 16 (bank spread)
 
+// Twiddles of one radix-2^r sub-butterfly: for the pass's stage st (global stage
+// s0 + st, distance d = D >> st) the 2^st groups it touches are
+// g = B0 / (2d) + t, t < 2^st (B0 = global start of its 2D block), i.e. the
+// entries k = 2^(s0+st) + (B0 >> (log2 D + 1 - st)) + t.  They do not depend on
+// the data, so each pass loads all of them (2^r - 1 pairs) before touching smem.
+
 // local forward passes over a chunk (global position of element 0 = c0), stages with
 // distance chunk/2 .. 1; s0 = global stage index of the first local stage
 template <int LOGC>
 __device__ __forceinline__ void fwd_local(uint64_t* sm, int64_t c0, int s0, const uint64_t* w, const uint64_t* ws,
                                           uint64_t p) {
-  constexpr int CH = 1 << LOGC, NT = CH / EPT;
+  constexpr int CH = 1 << LOGC;
   int done = 0;
   // first pass takes LOGC % 4 stages (if any), the rest are radix-16
 #pragma unroll
   for (int pass = 0; pass < (LOGC + 3) / 4; ++pass) {
     const int r = (pass == 0 && (LOGC % 4)) ? (LOGC % 4) : 4;
-    const int D = CH >> (done + 1);             // distance of the pass's first stage
+    const int logD = LOGC - done - 1;           // log2 distance of the pass's first stage
+    const int D = 1 << logD;
     const int inner = D >> (r - 1);             // stride between the 2^r elements
     const int per = EPT >> r;                   // independent sub-butterflies per thread
     uint64_t v[EPT];
     int base[EPT >> 1];
+    uint64_t tw[EPT >> 1][15], tws[EPT >> 1][15];
 #pragma unroll
     for (int h = 0; h < per; ++h) {
       const int id = threadIdx.x * per + h;
       const int b = id / inner, j = id - b * inner;
       base[h] = b * 2 * D + j;
+      const int64_t B0 = c0 + (int64_t)b * 2 * D;
+#pragma unroll
+      for (int st = 0; st < r; ++st) {
+        const int64_t k0 = ((int64_t)1 << (s0 + done + st)) + (B0 >> (logD + 1 - st));
+#pragma unroll
+        for (int t = 0; t < (1 << st); ++t) {
+          tw[h][(1 << st) - 1 + t] = __ldg(w + k0 + t);
+          tws[h][(1 << st) - 1 + t] = __ldg(ws + k0 + t);
+        }
+      }
 #pragma unroll
       for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = sm[pad(base[h] + lo * inner)];
     }
 #pragma unroll
     for (int st = 0; st < r; ++st) {
-      const int s = s0 + done + st;
-      const int d = D >> st;                    // distance in elements
       const int half = (1 << r) >> (st + 1);    // distance in lo units
 #pragma unroll
       for (int h = 0; h < per; ++h) {
 #pragma unroll
         for (int lo = 0; lo < (1 << r); ++lo) {
           if (lo & half) continue;
-          const int64_t gi = c0 + base[h] + lo * inner;   // global index of the upper element
-          const int64_t g = gi / (2 * d);
-          const int64_t k = ((int64_t)1 << s) + g;
-          ct_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], __ldg(w + k), __ldg(ws + k), p);
+          const int t = (1 << st) - 1 + (lo >> (r - st));
+          ct_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], tws[h][t], p);
         }
       }
     }
@@ -120,53 +153,65 @@ __device__ __forceinline__ void fwd_local(uint64_t* sm, int64_t c0, int s0, cons
     __syncthreads();
     done += r;
   }
-  (void)NT;
 }
 
 // local inverse passes: stages with distance 1 .. chunk/2 (global stage index s0 + LOGC - 1 .. s0)
 template <int LOGC>
 __device__ __forceinline__ void inv_local(uint64_t* sm, int64_t c0, int s0, const uint64_t* w, const uint64_t* ws,
-                                          uint64_t p) {
-  constexpr int CH = 1 << LOGC;
+                                          uint64_t p, uint64_t mu) {
   int done = 0;  // stages done, counted from distance 1 upwards
 #pragma unroll
   for (int pass = 0; pass < (LOGC + 3) / 4; ++pass) {
     const int r = (pass == (LOGC + 3) / 4 - 1 && (LOGC % 4)) ? (LOGC % 4) : 4;
     const int Dmin = 1 << done;               // distance of the pass's first (smallest) stage
-    const int D = Dmin << (r - 1);            // largest distance in the pass
+    const int logD = done + r - 1;            // log2 of the largest distance in the pass
+    const int D = 1 << logD;
     const int inner = Dmin;
     const int per = EPT >> r;
     uint64_t v[EPT];
     int base[EPT >> 1];
+    uint64_t tw[EPT >> 1][15], tws[EPT >> 1][15];
 #pragma unroll
     for (int h = 0; h < per; ++h) {
       const int id = threadIdx.x * per + h;
       const int b = id / inner, j = id - b * inner;
       base[h] = b * 2 * D + j;
+      const int64_t B0 = c0 + (int64_t)b * 2 * D;
+      // stage with distance D >> u (u = r-1-st) has 2^u groups in the block
+#pragma unroll
+      for (int u = 0; u < r; ++u) {
+        const int s = s0 + LOGC - 1 - (done + r - 1 - u);
+        const int64_t k0 = ((int64_t)1 << s) + (B0 >> (logD + 1 - u));
+#pragma unroll
+        for (int t = 0; t < (1 << u); ++t) {
+          tw[h][(1 << u) - 1 + t] = __ldg(w + k0 + t);
+          tws[h][(1 << u) - 1 + t] = __ldg(ws + k0 + t);
+        }
+      }
 #pragma unroll
       for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = sm[pad(base[h] + lo * inner)];
     }
 #pragma unroll
     for (int st = 0; st < r; ++st) {
-      const int d = Dmin << st;
       const int half = 1 << st;
-      const int s = s0 + LOGC - 1 - (done + st);
+      const int u = r - 1 - st;
 #pragma unroll
       for (int h = 0; h < per; ++h) {
 #pragma unroll
         for (int lo = 0; lo < (1 << r); ++lo) {
           if (lo & half) continue;
-          const int64_t gi = c0 + base[h] + lo * inner;
-          const int64_t g = gi / (2 * d);
-          const int64_t k = ((int64_t)1 << s) + g;
-          gs_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], __ldg(w + k), __ldg(ws + k), p);
+          const int t = (1 << u) - 1 + (lo >> (st + 1));
+          // inputs of stage st are < 2^(st+1) p (sums double, Shoup outputs < 2p)
+          gs_bfly_lazy(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], tws[h][t], p,
+                       p << (st + 1));
         }
       }
     }
 #pragma unroll
     for (int h = 0; h < per; ++h)
 #pragma unroll
-      for (int lo = 0; lo < (1 << r); ++lo) sm[pad(base[h] + lo * inner)] = v[h * (1 << r) + lo];
+      for (int lo = 0; lo < (1 << r); ++lo)
+        sm[pad(base[h] + lo * inner)] = barrett2(v[h * (1 << r) + lo], p, mu);
     __syncthreads();
     done += r;
   }
@@ -177,10 +222,15 @@ __device__ __forceinline__ uint64_t reduce4(uint64_t x, uint64_t p) {
   if (x >= p) x -= p;
   return x;
 }
+// x < 2^63 -> x mod p, with mu = floor(2^64 / p)
+__device__ __forceinline__ uint64_t reduce_full(uint64_t x, uint64_t p, uint64_t mu) {
+  uint64_t r = x - __umul64hi(x, mu) * p;  // [0, 2p)
+  return r >= p ? r - p : r;
+}
 
 // grid: (batch * L) clusters of C CTAs; data (batch, L, N) u64
 template <int LOGN, int LOGCL>
-__global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT) ntt_fwd_kernel(uint64_t* data, int L, Tables t) {
+__global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd_kernel(uint64_t* data, int L, Tables t) {
   constexpr int C = 1 << LOGCL, LOGC = LOGN - LOGCL, CH = 1 << LOGC, NT = CH / EPT;
   extern __shared__ __align__(16) uint64_t sm[];
   const int64_t poly = blockIdx.x / C;
@@ -196,7 +246,10 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT) ntt_fwd_kernel(ui
   } else {
     // cross-chunk stages 0 .. LOGCL-1: this CTA owns chunk offsets [c*CH/C, (c+1)*CH/C)
     cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();  // every peer is running before its shared memory is written
+    // every peer must be running before its shared memory is written: arrive now,
+    // wait just before the first remote store
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    bool waited = false;
     for (int o = c * (CH / C) + threadIdx.x; o < (c + 1) * (CH / C); o += NT) {
       uint64_t v[C];
 #pragma unroll
@@ -212,18 +265,24 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT) ntt_fwd_kernel(ui
           ct_bfly(v[q], v[q + half], __ldg(w + k), __ldg(ws + k), p);
         }
       }
+      if (!waited) {
+        asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+        waited = true;
+      }
 #pragma unroll
       for (int q = 0; q < C; ++q) cluster.map_shared_rank(sm, q)[pad(o)] = v[q];
     }
+    if (!waited) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     cluster.sync();
   }
   fwd_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, ws, p);
   uint64_t* xo = x + (int64_t)c * CH;
-  for (int i = threadIdx.x; i < CH; i += NT) xo[i] = reduce4(sm[pad(i)], p);
+  const uint64_t mu = t.mu[limb];
+  for (int i = threadIdx.x; i < CH; i += NT) xo[i] = reduce_full(sm[pad(i)], p, mu);
 }
 
 template <int LOGN, int LOGCL>
-__global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT) ntt_inv_kernel(uint64_t* data, int L, Tables t) {
+__global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_inv_kernel(uint64_t* data, int L, Tables t) {
   constexpr int C = 1 << LOGCL, LOGC = LOGN - LOGCL, CH = 1 << LOGC, NT = CH / EPT;
   extern __shared__ __align__(16) uint64_t sm[];
   const int64_t poly = blockIdx.x / C;
@@ -240,7 +299,7 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT) ntt_inv_kernel(ui
     sm[pad(i)] = v >= p ? v - p : v;  // tolerate inputs in [0, 2p)
   }
   __syncthreads();
-  inv_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, ws, p);
+  inv_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, ws, p, t.mu[limb]);
   if (C == 1) {
     for (int i = threadIdx.x; i < CH; i += NT) x[i] = reduce4(shoup(sm[pad(i)], ninv, ninvs, p), p);
   } else {
@@ -369,7 +428,8 @@ int sfhr_ntt_plan_create(int logn, int L, int prime_bits, int device, sfhr_ntt_p
   if (!out) return nfail(SFHR_EINVAL, "null output");
   if (logn < 10 || logn > 16) return nfail(SFHR_EINVAL, "log2 N must be in [10, 16]");
   if (L < 1 || L > 32) return nfail(SFHR_EINVAL, "limb count must be in [1, 32]");
-  if (prime_bits < 30 || prime_bits > 61) return nfail(SFHR_EINVAL, "prime bits must be in [30, 61]");
+  // the lazy forward butterflies keep values below (2 log2 N + 1) p < 2^56 (see ct_bfly)
+  if (prime_bits < 30 || prime_bits > 50) return nfail(SFHR_EINVAL, "prime bits must be in [30, 50]");
   auto* P = new sfhr_ntt_plan();
   P->logn = logn;
   P->L = L;
@@ -418,7 +478,7 @@ int sfhr_ntt_plan_create(int logn, int L, int prime_bits, int device, sfhr_ntt_p
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
-    const size_t words = (size_t)4 * L * N + L;
+    const size_t words = (size_t)4 * L * N + 2 * L;
     cudaError_t e = cudaMalloc(&P->d_tab, words * 8);
     uint64_t* d = P->d_tab;
     if (e == cudaSuccess) e = cudaMemcpy(d, P->w.data(), L * N * 8, cudaMemcpyHostToDevice);
@@ -426,13 +486,16 @@ int sfhr_ntt_plan_create(int logn, int L, int prime_bits, int device, sfhr_ntt_p
     if (e == cudaSuccess) e = cudaMemcpy(d + 2 * L * N, P->wi.data(), L * N * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d + 3 * L * N, P->wis.data(), L * N * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(d + 4 * L * N, P->primes.data(), L * 8, cudaMemcpyHostToDevice);
+    std::vector<uint64_t> mus(L);
+    for (int i = 0; i < L; ++i) mus[i] = (uint64_t)(((unsigned __int128)1 << 64) / P->primes[i]);
+    if (e == cudaSuccess) e = cudaMemcpy(d + 4 * L * N + L, mus.data(), L * 8, cudaMemcpyHostToDevice);
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
       cudaFree(P->d_tab);
       delete P;
       return nfail(SFHR_ECUDA, std::string("ntt tables: ") + cudaGetErrorString(e));
     }
-    P->t = Tables{d, d + L * N, d + 2 * L * N, d + 3 * L * N, d + 4 * L * N};
+    P->t = Tables{d, d + L * N, d + 2 * L * N, d + 3 * L * N, d + 4 * L * N, d + 4 * L * N + L};
   }
   *out = P;
   return SFHR_OK;
