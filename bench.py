@@ -39,6 +39,11 @@ sys.path.insert(0, str(ROOT))
 
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 METRIC = "ct-ops/s (key switches per second), ResNet-20-shape server inference"
+
+
+def metric_for(workload):
+    return METRIC if workload == "resnet20" else \
+        f"ct-ops/s (key switches per second), {WORKLOADS[workload][0].split(' (')[0]}"
 UNIT = "key-switches/s"
 
 
@@ -48,12 +53,37 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--b", type=int, default=12)
-    ap.add_argument("--gamma", type=int, default=0)
+    ap.add_argument("--b", type=int, default=None)
+    ap.add_argument("--gamma", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
-    return ap.parse_args()
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="resnet20",
+                    help="BASELINE configs: mlp = [0], resnet20 = [2] (default, the metric's config), "
+                         "resnet18 = [3], resnet34 = [4] (one request per GPU)")
+    a = ap.parse_args()
+    if a.b is None:
+        a.b = WORKLOADS[a.workload][1]
+    if a.gamma is None:
+        a.gamma = WORKLOADS[a.workload][2]
+    return a
+
+
+# workload -> (description, default b, default gamma, rounds label)
+WORKLOADS = {
+    "resnet20": ("ResNet-20-shape server inference (3x32x32, 10 classes)", 12, 0),
+    "mlp": ("hybrid MLP 784-128-10 server inference", 16, 0),
+    "resnet18": ("ResNet-18-shape server inference (3x64x64, 200 classes)", 16, 1),
+    "resnet34": ("ResNet-34-shape server inference (3x224x224, 1000 classes), one request", 16, 1),
+}
+
+
+def make_model(workload, b, seed):
+    from paper_2509_01253_b200 import workloads as W
+    if workload == "mlp":
+        return W.mlp_model(seed)
+    return {"resnet20": W.resnet20_model, "resnet18": W.resnet18_model,
+            "resnet34": W.resnet34_model}[workload](b, seed=seed)
 
 
 # ---------------------------------------------------------------------------
@@ -156,12 +186,10 @@ def run_ours(args, rank, world, local_rank):
     from paper_2509_01253_b200.engine import ServerEngine
     from paper_2509_01253_b200.keyswitch import KeySwitchKeySet
     from paper_2509_01253_b200.params import preset_for_bits
-    from paper_2509_01253_b200.workloads import resnet20_model
-
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     scheme = preset_for_bits(args.b, args.gamma)
-    model = resnet20_model(args.b, seed=args.seed)
+    model = make_model(args.workload, args.b, args.seed)
     R = scheme.ring
     engine = ServerEngine(model, scheme, master_seed=bytes(32), device=local_rank)
     keys = synthetic_ksk(scheme, args.seed)
@@ -264,7 +292,7 @@ def run_ours(args, rank, world, local_rank):
             tot = t.item()
         e2e = {"value": ks_all / tot, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "latency_s_per_inference": tot / args.steps,
-               "path": "ServerEngine.open_session + server_round x20 (host numpy bundles)"}
+               "path": f"ServerEngine.open_session + server_round x{len(model.rounds)} (host numpy bundles)"}
     clk = clocks.stop()
 
     # ---- roofline of the dominant kernel (fused key-switch stage) ----
@@ -281,11 +309,12 @@ def run_ours(args, rank, world, local_rank):
             "note": "INT-pipe bound at these ring sizes (SURVEY §8(d)); HBM fraction reported as required"}
 
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64 (mod 2^53) / u32 NTT residues",
-        "data": "synthetic uniform uploads of the exact per-round shapes; random-init quantized ResNet-20 weights",
-        "config": {"workload": f"ResNet-20-shape server inference (20 rounds), b={args.b} (M={R.M}), gamma={args.gamma}",
+        "data": "synthetic uniform uploads of the exact per-round shapes; random-init quantized weights",
+        "config": {"workload": f"{WORKLOADS[args.workload][0]}, {len(model.rounds)} rounds, b={args.b} "
+                               f"(M={R.M}), gamma={args.gamma}",
                    "key_switches_per_step": int(ks_per_step), "rounds": len(model.rounds),
                    "latency_s_per_inference": total_ms_max / args.steps / 1e3,
                    "l2": "256 MiB L2 flush between timed steps; per-step working set > L2",
@@ -331,8 +360,45 @@ def cpu_stem_round(args, model, scheme, powers, exps, keys, threads):
     return dt, st.key_switches
 
 
+def cpu_pack_sample(args, keys, n_groups, threads):
+    """Bounded CPU sample for the large workloads: fast_pack of n_groups full
+    pack groups of uniform rows (the reference's dominant phase)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import keyswitch as oks
+    from oracle import pack as opk
+    from oracle import scheme as osc
+    os_ = osc.preset(args.b, args.gamma)
+    R = os_.ring
+    ksk = oks.KskSet({d: [oks.Ct(c.a, c.b) for c in row] for d, row in keys.items()}, os_.gadget, 0.0, R)
+    eng = oks.KsEngine(ksk, "fft")
+    F = os_.pack_factor
+    rng = np.random.default_rng(5)
+    groups = [rng.integers(0, 1 << 53, (F, 2, R.N), dtype=np.uint64) for _ in range(n_groups)]
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(1)
+    except Exception:
+        lim = None
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(lambda g: opk.fast_pack(g, os_, eng), groups))
+    dt = time.perf_counter() - t0
+    if lim is not None:
+        lim.unregister()
+    ks = n_groups * opk.expected_pack_switches(R.t, R.alpha, os_.beta_eff, args.gamma)
+    return dt, ks
+
+
 def cpu_baseline(args, model, scheme, powers, exps, keys, sample_reps=1):
     cores = os.cpu_count() or 1
+    if args.workload in ("resnet18", "resnet34"):
+        n = 2 * cores
+        dt, ks = cpu_pack_sample(args, keys, n, cores)
+        return {"value": ks / dt, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": f"{n} full pack groups (fast_pack, fft key switching) of uniform rows, b={args.b} "
+                          f"gamma={args.gamma}, thread pool of {cores}; {ks} key switches in {dt:.2f} s "
+                          f"(extraction + linear excluded: full CPU rounds of this shape take hours)"}
     ts, ks = [], 0
     for _ in range(sample_reps):
         dt, k = cpu_stem_round(args, model, scheme, powers, exps, keys, cores)
@@ -346,28 +412,35 @@ def cpu_baseline(args, model, scheme, powers, exps, keys, sample_reps=1):
 
 def run_reference(args):
     from paper_2509_01253_b200.params import preset_for_bits
-    from paper_2509_01253_b200.workloads import resnet20_model
     scheme = preset_for_bits(args.b, args.gamma)
-    model = resnet20_model(args.b, seed=args.seed)
+    model = make_model(args.workload, args.b, args.seed)
     powers, exps = synthetic_inputs(model, scheme, args.seed + 1000)
     keys = synthetic_ksk(scheme, args.seed)
     cores = os.cpu_count() or 1
+    big = args.workload in ("resnet18", "resnet34")
+    one = (lambda: cpu_pack_sample(args, keys, 2 * cores, cores)) if big else \
+        (lambda: cpu_stem_round(args, model, scheme, powers[:1], exps, keys, cores))
     for _ in range(args.warmup):
-        cpu_stem_round(args, model, scheme, powers[:1], exps, keys, cores)
+        one()
     ts, ks = [], 0
     for _ in range(args.steps):
-        dt, k = cpu_stem_round(args, model, scheme, powers[:1], exps, keys, cores)
+        dt, k = one()
         ts.append(dt)
         ks += k
     value = ks / sum(ts)
-    sample = (f"ResNet-20 stem round (3072->16384 rows, 56 packs), b={args.b} gamma={args.gamma}, "
+    r0 = model.rounds[0]
+    sample = (f"{args.workload} first round ({r0.input_len}->{r0.output_len} rows), b={args.b} gamma={args.gamma}, "
               f"oracle port of the reference CPU path (fft KS), {cores} threads")
-    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    if big:
+        sample = (f"{2 * cores} full pack groups per step (fast_pack, fft KS) of uniform rows, b={args.b} "
+                  f"gamma={args.gamma}, {cores} threads (extraction + linear excluded)")
+    return {"impl": "reference", "metric": metric_for(args.workload), "value": value, "unit": UNIT,
+            "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(ts) / len(ts),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "u64 (mod 2^53) / f64 FFT", "data": "synthetic",
-            "config": {"workload": f"ResNet-20-shape server inference (20 rounds), b={args.b} (M={scheme.ring.M}), "
-                                   f"gamma={args.gamma}", "sample": "stem round"},
+            "config": {"workload": f"{WORKLOADS[args.workload][0]}, {len(model.rounds)} rounds, b={args.b} "
+                                   f"(M={scheme.ring.M}), gamma={args.gamma}", "sample": "first (stem) round"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
