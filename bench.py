@@ -296,11 +296,13 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
 
     # ---- roofline of the dominant kernel (fused key-switch stage) ----
+    traffic = stage_traffic(R.N)
     peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
     achieved = (ks_bytes / (ks_ms / 1e3)) / 1e9 if ks_ms > 0 else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": (achieved / hbm) if achieved else None, "traffic": None,
+            "frac": (achieved / hbm) if achieved else None,
+            "traffic": traffic.get("traffic"), "traffic_detail": traffic,
             "kernel": "ks_stage_kernel (fused automorphism+decompose+Phi_M-NTT key switch+CRT)",
             "algorithmic_bytes": "rows * 32 * N per launch (read a,b; write a',b')",
             "launches_timed": ks_launches, "kernel_ms_per_step": ks_ms / args.steps,
@@ -324,6 +326,27 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, model, scheme, powers, exps, keys, sample_reps=1)
     return line
+
+
+def stage_traffic(N):
+    """DRAM bytes per ks_stage_kernel launch from the committed `ncu --set full` capture.
+
+    Returned per launch (mean over the captured launches), with the ratio to the
+    algorithmic 32 N bytes per row (rows = grid / 3 CTAs per cluster); the capture
+    is of the b = 12 (N = 2058) ResNet-20 stem pack, so the ratio is only quoted
+    for that ring."""
+    f = ROOT / "profiles" / "r01_ncu_stage_v8_summary.json"
+    try:
+        launches = [l for l in json.loads(f.read_text())["launches"] if "ks_stage_kernel" in l["kernel"]]
+    except Exception:
+        return {"traffic": None, "note": f"{f.name} missing"}
+    tr = [1e6 * (l["dram__bytes_read.sum"] + l["dram__bytes_write.sum"]) for l in launches]
+    alg = [l["launch__grid_size"] / 3 * 32 * 2058 for l in launches]
+    out = {"traffic": sum(tr) / len(tr), "unit": "bytes per launch", "launches": len(tr),
+           "algorithmic_bytes_per_launch": sum(alg) / len(alg), "source": f"profiles/{f.name}"}
+    if N == 2058:
+        out["traffic_over_algorithmic"] = sum(tr) / sum(alg)
+    return out
 
 
 # ---------------------------------------------------------------------------
