@@ -515,13 +515,22 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   cluster.sync();
 }
 
+#ifndef SFHR_T7_THREADS
+#define SFHR_T7_THREADS 352
+#endif
+#ifndef SFHR_T5_THREADS
+#define SFHR_T5_THREADS 512
+#endif
+#ifndef SFHR_T5_MINBLOCKS
+#define SFHR_T5_MINBLOCKS 2
+#endif
 #ifndef SFHR_T7_MINBLOCKS
 #define SFHR_T7_MINBLOCKS 3
 #endif
 template <int T>
 struct StageLaunch {
-  static constexpr int kThreads = T == 7 ? 352 : 512;
-  static constexpr int kMinBlocks = T == 7 ? SFHR_T7_MINBLOCKS : 2;
+  static constexpr int kThreads = T == 7 ? SFHR_T7_THREADS : T == 5 ? SFHR_T5_THREADS : 512;
+  static constexpr int kMinBlocks = T == 7 ? SFHR_T7_MINBLOCKS : T == 5 ? SFHR_T5_MINBLOCKS : 2;
 };
 
 template <int T, int A, int L>
@@ -595,8 +604,12 @@ size_t stage_smem_bytes(const RingConst& rc) {
 }
 
 int stage_threads(const RingConst& rc) {
-  const int cap = rc.t == 7 ? StageLaunch<7>::kThreads : StageLaunch<5>::kThreads;
+  const int cap = rc.t == 7 ? StageLaunch<7>::kThreads : rc.t == 5 ? StageLaunch<5>::kThreads
+                                                                    : StageLaunch<3>::kThreads;
   const int need = ((rc.nitems + 31) / 32) * 32;
+  const bool production = (rc.t == 7 && rc.alpha == 4) || (rc.t == 5 && rc.alpha == 5) ||
+                          (rc.t == 3 && rc.alpha == 7);
+  if (production && cap >= need) return cap;  // the tuned block size of the compile-time geometry
   // enough threads for one pass over the n1 first-step columns when they fit
   const int want = ((rc.n1 + 31) / 32) * 32;
   return want <= cap ? (want > need ? want : need) : need;

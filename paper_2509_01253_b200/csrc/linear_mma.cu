@@ -35,7 +35,8 @@ constexpr int PRODUCERS = 128;            // cp.async gather threads
 constexpr int MMA_THREADS = EPI_WARPS * 32 + PRODUCERS + 32;
 constexpr int KC = 64;                    // taps per pipeline stage (2 MMAs)
 constexpr int NSTAGE = 4;
-constexpr int STAGE_BYTES = KC * 128;     // 8 KB
+constexpr int STAGE_BYTES = KC * 128;     // 8 KB of A per stage
+constexpr int B_RESIDENT_MAX = 96 * 1024; // larger weight operands are streamed with each stage
 constexpr int EP_COLS = 16;               // accumulator columns per epilogue chunk
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -113,12 +114,16 @@ __device__ __forceinline__ uint64_t sx(int v) { return (uint64_t)(int64_t)v; }
 
 // byte offsets of the dynamic shared-memory carve-up (host and device agree)
 struct MmaSmem {
-  int ring, b, ep, colp, odst, ocan, bars, tslot, total;
+  int ring, stage, bstage, b, ep, colp, odst, ocan, bars, tslot, total;
+  bool stream;  // B streamed per stage (stage = A 8 KB + B chunk Np x 64 B) instead of resident
   __host__ __device__ static MmaSmem make(int Np, int Kp) {
     MmaSmem s;
+    s.stream = Np * Kp > B_RESIDENT_MAX;
     s.ring = 0;
-    s.b = s.ring + NSTAGE * STAGE_BYTES;
-    s.ep = s.b + ((Np * Kp + 127) & ~127);
+    s.bstage = s.stream ? Np * KC : 0;
+    s.stage = STAGE_BYTES + s.bstage;  // multiple of 1024 (Np % 16 == 0)
+    s.b = s.ring + NSTAGE * s.stage;
+    s.ep = s.b + (s.stream ? 0 : ((Np * Kp + 127) & ~127));
     s.colp = s.ep + EPI_WARPS * EP_COLS * 32 * 4;
     s.odst = s.colp + Kp * 8;
     s.ocan = s.odst + Np * 8;
@@ -149,6 +154,7 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   unsigned char* sm = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   const MmaSmem L = MmaSmem::make(Np, Kp);
   const uint32_t ring = su32(sm + L.ring), bsm = su32(sm + L.b);
+  const int SB = L.stage;  // bytes per pipeline stage
   const unsigned char** colp = reinterpret_cast<const unsigned char**>(sm + L.colp);
   int64_t* odst = reinterpret_cast<int64_t*>(sm + L.odst);
   int32_t* ocan = reinterpret_cast<int32_t*>(sm + L.ocan);
@@ -161,7 +167,8 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
 
   // ---- setup: B operand (weights), tap row pointers, output row maps, barriers, TMEM ----
   const unsigned char* wsrc = a.tw + w0;
-  for (int i = tid; i < Np * Kp / 16; i += MMA_THREADS) cp16(bsm + 16 * i, wsrc + 16 * i, 16);
+  if (!L.stream)
+    for (int i = tid; i < Np * Kp / 16; i += MMA_THREADS) cp16(bsm + 16 * i, wsrc + 16 * i, 16);
   cp_commit();
   const unsigned char* in8 = reinterpret_cast<const unsigned char*>(a.in);
   const unsigned char* rin8 = reinterpret_cast<const unsigned char*>(a.round_in);
@@ -225,7 +232,13 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
         mbar_wait(empty0 + 8 * stage, phase ^ 1);
         const int ntaps = min(KC, Kp - kc * KC);
         const unsigned char* const* cp = colp + kc * KC;
-        const uint32_t dst = ring + stage * STAGE_BYTES + dst_lane;
+        const uint32_t dst = ring + stage * SB + dst_lane;
+        if (L.stream) {  // this stage's B chunk: K blocks 4kc.. of the packed [K/16][N/8][8][16] weights
+          const int kb0 = kc * (KC / 16), nkb = min(KC, Kp - kc * KC) / 16;
+          const unsigned char* bsrc = wsrc + (size_t)kb0 * (Np / 8) * 128;
+          const uint32_t bdst = ring + stage * SB + STAGE_BYTES;
+          for (int i = pt; i < nkb * (Np / 8) * 8; i += PRODUCERS) cp16(bdst + 16 * i, bsrc + 16 * i, 16);
+        }
 #pragma unroll
         for (int i = 0; i < KC / 16; ++i) {
           const int tap = tb + 16 * i;
@@ -260,9 +273,10 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
         if (lane == 0) {
           const int nmma = min(KC, Kp - kc * KC) / 32;
           for (int j = 0; j < nmma; ++j) {
-            const uint64_t ad = sdesc(ring + stage * STAGE_BYTES + j * 4096, 16, 1024, 2);
-            const int kb = (kc * KC + j * 32) >> 4;
-            const uint64_t bd = sdesc(bsm + kb * b_kblock, b_kblock, 128, 0);
+            const uint64_t ad = sdesc(ring + stage * SB + j * 4096, 16, 1024, 2);
+            const uint64_t bd = L.stream
+                                    ? sdesc(ring + stage * SB + STAGE_BYTES + 2 * j * b_kblock, b_kblock, 128, 0)
+                                    : sdesc(bsm + ((kc * KC + j * 32) >> 4) * b_kblock, b_kblock, 128, 0);
             mma_i8(tmem + (uint32_t)(buf * Np), ad, bd, idesc, (kc > 0 || j > 0) ? 1u : 0u);
           }
           mma_commit(empty0 + 8 * stage);
@@ -319,7 +333,12 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
 }
 
 size_t linear_mma_smem_bytes(int Np, int Kp) {
-  return (size_t)MmaSmem::make(Np, Kp).total;
+  // worst case over the tiles of a launch (N_pad <= Np, K_pad <= Kp): the streamed layout of
+  // (Np, Kp) and any resident layout (B <= B_RESIDENT_MAX) with the same colp / row tables
+  const MmaSmem s = MmaSmem::make(Np, Kp);
+  const size_t bres = (size_t)Np * Kp < (size_t)B_RESIDENT_MAX ? (size_t)Np * Kp : (size_t)B_RESIDENT_MAX;
+  const size_t resident = (size_t)NSTAGE * STAGE_BYTES + ((bres + 127) & ~(size_t)127) + (s.total - s.ep);
+  return s.total > resident ? (size_t)s.total : resident;
 }
 
 cudaError_t launch_linear_mma(const LinearMmaArgs& a, int max_np, int max_kp, cudaStream_t st) {

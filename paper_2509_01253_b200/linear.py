@@ -22,7 +22,7 @@ from .model import ROWS_PER_GROUP, LinearPass, ModelError
 
 _LIMB = 18
 MMA_MAX_ROWS = 256      # N of one tcgen05 tile group
-MMA_MAX_BYTES = 150 * 1024  # s8 weights of a tile group kept in shared memory
+MMA_MAX_KPAD = 8192     # taps per tile group (row-pointer table in shared memory)
 MMA_ENABLED = os.environ.get("SFHR_LINEAR_MMA", "1") != "0"
 
 
@@ -108,7 +108,7 @@ def split_mma_tiles(ps: LinearPass):
                                  .reshape(nc, ROWS_PER_GROUP)[:, :int(g[q][4])].T for q in run])
             if ex_vals is not None:
                 wt = np.concatenate([wt, ex_vals], axis=1)
-            if np.abs(wt).max(initial=0) > 127 or n_pad * k_pad > MMA_MAX_BYTES or len(ex_cols) > 256:
+            if np.abs(wt).max(initial=0) > 127 or k_pad > MMA_MAX_KPAD or len(ex_cols) > 256:
                 rest.extend(run)
                 i = j
                 continue

@@ -101,7 +101,9 @@ def test_tiles_cover_rows_once_and_replay_exactly(name):
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
 @pytest.mark.parametrize("shape", [(1, 1, 2), (16, 32, 16), (17, 33, 18), (300, 45, 30), (5, 700, 2),
-                                   (64, 576, 4116), (128, 784, 100)])
+                                   (64, 576, 4116), (128, 784, 100),
+                                   # streamed weight operands (N_pad x K_pad > 96 KB)
+                                   (256, 576, 100), (64, 4608, 18), (200, 1000, 34)])
 def test_mma_matmul_matches_oracle(shape):
     e_out, e_in, lanes = shape
     rng = np.random.default_rng(sum(shape))
@@ -118,14 +120,16 @@ def test_mma_matmul_matches_oracle(shape):
 
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
-@pytest.mark.parametrize("r", [0, 1, 2, 7, 13, 19])
-def test_mma_round_matches_cuda_core_kernel(r, monkeypatch):
-    """A full ResNet-20 round map (maps, residual extras, bias) through both kernels."""
+@pytest.mark.parametrize("net,r", [("r20", 0), ("r20", 1), ("r20", 2), ("r20", 7), ("r20", 13), ("r20", 19),
+                                   ("r18", 1), ("r18", 12), ("r18", 15), ("r18", 16)])
+def test_mma_round_matches_cuda_core_kernel(net, r, monkeypatch):
+    """A full ResNet round map (maps, residual extras, bias) through both kernels."""
     import torch
     from paper_2509_01253_b200.device import RingContext
     from paper_2509_01253_b200.params import preset_for_bits
-    model = W.resnet20_model(12, 0)
-    sch = preset_for_bits(12, 0)
+    b = 12 if net == "r20" else 16
+    model = W.resnet20_model(12, 0) if net == "r20" else W.resnet18_model(16, 0)
+    sch = preset_for_bits(b, 0)
     R = sch.ring
     ctx = RingContext.get(R.t, R.alpha, R.p_bits, sch.gadget.D, sch.gadget.l, 0, sch.beta, 0)
     rnd = model.rounds[r]
@@ -142,7 +146,7 @@ def test_mma_round_matches_cuda_core_kernel(r, monkeypatch):
     for enabled in (True, False):
         monkeypatch.setattr(lin, "MMA_ENABLED", enabled)
         dps = [lin.DevicePass(p, ctx.dev) for p in passes]
-        assert (dps[0].n_mma_tiles > 0) == enabled or r == 19
+        assert any(dp.n_mma_tiles > 0 for dp in dps) == enabled
         out = torch.zeros((rnd.output_len, 2, R.N), dtype=torch.int64, device=ctx.dev)
         lin.run_round(ctx, dps, x, in_map, out, out_map, unit)
         torch.cuda.synchronize()
