@@ -106,8 +106,75 @@ __global__ void extract_kernel(const __grid_constant__ RingConst rc, const __gri
   }
 }
 
+// Row-tiled variant: one CTA per (chunk, EX_ROWS consecutive coefficients), the chunk's
+// power ciphertexts staged once in shared memory (zero beyond N, so the reference's
+// masked reads become plain reads), per-(row, power) rotation offsets precomputed, every
+// thread producing 2N / EX_THREADS lanes of each row.  HBM-write-bound.
+constexpr int EX_ROWS = 32;
+constexpr int EX_THREADS = 512;
+constexpr int EX_MAXPOW = 8;
+
+__global__ void __launch_bounds__(EX_THREADS) extract_tiled_kernel(const __grid_constant__ RingConst rc,
+                                                                   const __grid_constant__ ExtractArgs a) {
+  extern __shared__ __align__(16) uint64_t sp[];  // [npow][2][M]
+  __shared__ uint32_t sid[EX_ROWS][EX_MAXPOW], ssh[EX_ROWS][EX_MAXPOW];
+  const int N = rc.N, M = rc.M, n1 = rc.n1;
+  const int rblocks = (N + EX_ROWS - 1) / EX_ROWS;
+  const int j = (int)(blockIdx.x / rblocks), rb = (int)(blockIdx.x % rblocks);
+  const int i0 = rb * EX_ROWS;
+  const int64_t g0 = (int64_t)j * N + i0;
+  if (g0 >= a.E) return;
+  const int nrows = (int)min((int64_t)min(EX_ROWS, N - i0), a.E - g0);
+  const int np = a.npow;
+  const uint64_t* src = a.power + (int64_t)j * np * 2 * N;
+  for (int idx = threadIdx.x; idx < np * 2 * M; idx += EX_THREADS) {
+    const int qc = idx / M, x = idx - qc * M;
+    sp[idx] = x < N ? src[(int64_t)qc * N + x] : 0ull;
+  }
+  for (int t = threadIdx.x; t < nrows * np; t += EX_THREADS) {
+    const int r = t / np, q = t - r * np;
+    const uint32_t d = a.exps[q];
+    sid[r][q] = fastmod((uint32_t)(i0 + r) * d, M, rc.magicM);
+    ssh[r][q] = fastmod((uint32_t)(a.cvec[i0 + r] * n1) * d, M, rc.magicM);
+  }
+  __syncthreads();
+  for (int r = 0; r < nrows; ++r) {
+    uint64_t* dst = a.rows + (g0 + r) * 2 * N;
+    for (int lane = threadIdx.x; lane < 2 * N; lane += EX_THREADS) {
+      const int comp = lane >= N;
+      const int k = lane - comp * N;
+      const uint32_t km = fastmod((uint32_t)k, n1, rc.magicN1);
+      uint64_t acc = 0;
+      for (int q = 0; q < np; ++q) {
+        const uint64_t* ct = sp + (2 * q + comp) * M;
+        const uint32_t id = sid[r][q], sh = ssh[r][q];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t x = id + (h ? (uint32_t)(N + km) : (uint32_t)k);
+          x = x >= (uint32_t)M ? x - M : x;
+          x = x >= (uint32_t)M ? x - M : x;
+          const uint32_t y = x >= sh ? x - sh : x + M - sh;
+          const uint64_t t = ct[x] - ct[y];
+          acc = h ? acc - t : acc + t;
+        }
+      }
+      dst[lane] = (acc * a.cu) & QMASK;
+    }
+  }
+}
+
+size_t extract_tiled_smem(const RingConst& rc, int npow) { return (size_t)npow * 2 * rc.M * 8; }
+
 cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
   if (a.E == 0) return cudaSuccess;
+  const size_t smem = extract_tiled_smem(rc, a.npow);
+  if (a.npow <= EX_MAXPOW && smem <= 200 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(extract_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int rblocks = (rc.N + EX_ROWS - 1) / EX_ROWS;
+    extract_tiled_kernel<<<(unsigned)(a.k_chunks * rblocks), EX_THREADS, smem, st>>>(rc, a);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)a.E, (2 * rc.N + 255) / 256);
   extract_kernel<<<grid, 256, 0, st>>>(rc, a);
   return cudaGetLastError();
