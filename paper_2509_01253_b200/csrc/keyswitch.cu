@@ -516,7 +516,7 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
 }
 
 #ifndef SFHR_T7_THREADS
-#define SFHR_T7_THREADS 352
+#define SFHR_T7_THREADS 384
 #endif
 #ifndef SFHR_T5_THREADS
 #define SFHR_T5_THREADS 512
