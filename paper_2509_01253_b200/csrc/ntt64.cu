@@ -8,11 +8,11 @@
 // and bit-exactly against the plain-C oracle in oracle/ntt_ref.c.
 //
 // Algorithm: merged-twiddle Cooley-Tukey forward (natural order in,
-// bit-reversed out; twiddles psi^brv(k)) and Gentleman-Sande inverse with Shoup
-// multiplication (w' = floor(w 2^64 / p)).  Primes are < 2^50, so the 14 spare
-// bits of a u64 let the butterflies run without range corrections (forward:
-// values < (2 log2 N + 1) p; inverse: sums reduced once per radix-16 pass);
-// residues are fully reduced at the boundary.
+// bit-reversed out; twiddles psi^brv(k)) and Gentleman-Sande inverse.  The
+// modular arithmetic runs on the FP64 pipe: residues (< 2^50) are exact integers
+// in doubles, x w mod p = (h + l) - rint(x w/p) p with the FMA error-free product
+// h + l (see mulmod_d; exact for |x| < 2^52), values kept below 4p by a rounding
+// reduction every two stages; u64 residues in and out, fully reduced.
 //
 // One HBM pass per transform: a polynomial is split over a thread-block
 // CLUSTER of C = max(1, N / 8192) CTAs, each holding a contiguous chunk of
@@ -46,47 +46,45 @@ constexpr int EPT = 16;          // residues per thread in a local pass
 #endif
 
 struct Tables {
-  const uint64_t* w;    // [L][N] psi^brv(k) (forward), k >= 1 used
-  const uint64_t* ws;   // [L][N] Shoup companions
-  const uint64_t* wi;   // [L][N] psi^-brv(k) (inverse); wi[0] = N^-1
-  const uint64_t* wis;  // [L][N]
-  const uint64_t* p;    // [L]
-  const uint64_t* mu;   // [L] floor(2^64 / p)
+  const double* w;     // [L][N] psi^brv(k) (forward), k >= 1 used, exact integers
+  const double* wp;    // [L][N] w / p (rounded)
+  const double* wi;    // [L][N] psi^-brv(k) (inverse); wi[0] = N^-1
+  const double* wip;   // [L][N]
+  const uint64_t* p;   // [L]
 };
 
-__device__ __forceinline__ uint64_t shoup(uint64_t x, uint64_t w, uint64_t ws, uint64_t p) {
-  const uint64_t q = __umul64hi(x, ws);
-  return x * w - q * p;  // in [0, 2p) for any x < 2^64
+// Modular arithmetic on the FP64 pipe (B200: ~60 DFMA/clk/SM vs ~7 64-bit mulhi/clk/SM).
+// Residues are exact integers held in doubles, |x| < 2^52 (primes < 2^50, values < 4p).
+// mulmod: h + l = x w exactly (FMA error-free product), q = rint(x w/p) is within 1.5
+// of x w / p, and h - q p is an integer below 2^53, so fma(-q, p, h) is exact and
+// r = x w - q p exactly, |r| <= 1.5 p.  (Intrinsics keep the compiler from contracting.)
+__device__ __forceinline__ double mulmod_d(double x, double w, double wp, double p) {
+  const double h = __dmul_rn(x, w);
+  const double l = __fma_rn(x, w, -h);
+  const double q = rint(__dmul_rn(x, wp));
+  return __dadd_rn(__fma_rn(-q, p, h), l);
 }
-
-// forward CT butterfly without range corrections: Shoup accepts any 64-bit Y and
-// returns t in [0, 2p), so an input bound X, Y < k p gives outputs < (k + 2) p.
-// After the 16 stages of N = 2^16 every value is < 33 p < 2^56 (p < 2^50 is
-// enforced by the planner), and one final reduction brings it to [0, p).
-__device__ __forceinline__ void ct_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t p) {
-  const uint64_t t = shoup(Y, w, ws, p);
-  const uint64_t x = X;
-  X = x + t;
-  Y = x + (2 * p - t);
+// |x| < 2^52 -> x mod p in [-p/2, p/2] (up to rounding of x / p)
+__device__ __forceinline__ double red_d(double x, double p, double pinv) {
+  return __fma_rn(-rint(__dmul_rn(x, pinv)), p, x);
 }
-// inverse GS butterfly with lazy sums: X, Y < M (M a multiple of p) -> X' = X + Y < 2M,
-// Y' in [0, 2p); a local pass reduces once at its end
-__device__ __forceinline__ void gs_bfly_lazy(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t p,
-                                             uint64_t M) {
-  const uint64_t x = X, y = Y;
-  X = x + y;
-  Y = shoup(x + M - y, w, ws, p);
+__device__ __forceinline__ uint64_t to_residue(double x, double p, double pinv) {
+  double r = red_d(x, p, pinv);
+  if (r < 0.0) r = __dadd_rn(r, p);
+  return (uint64_t)r;
 }
-__device__ __forceinline__ uint64_t barrett2(uint64_t x, uint64_t p, uint64_t mu) {
-  return x - __umul64hi(x, mu) * p;  // x < 2^63 -> [0, 2p)
+// forward CT butterfly: |X|, |Y| < B -> |X'|, |Y'| < B + 1.5 p
+__device__ __forceinline__ void ct_bfly(double& X, double& Y, double w, double wp, double p) {
+  const double t = mulmod_d(Y, w, wp, p);
+  const double x = X;
+  X = __dadd_rn(x, t);
+  Y = __dsub_rn(x, t);
 }
-// inverse GS butterfly, inputs/outputs in [0, 2p)
-__device__ __forceinline__ void gs_bfly(uint64_t& X, uint64_t& Y, uint64_t w, uint64_t ws, uint64_t p) {
-  const uint64_t p2 = 2 * p;
-  const uint64_t x = X, y = Y;
-  uint64_t s = x + y;
-  X = s >= p2 ? s - p2 : s;
-  Y = shoup(x - y + p2, w, ws, p);
+// inverse GS butterfly: X' = X + Y, Y' = (X - Y) w
+__device__ __forceinline__ void gs_bfly(double& X, double& Y, double w, double wp, double p) {
+  const double x = X, y = Y;
+  X = __dadd_rn(x, y);
+  Y = mulmod_d(__dsub_rn(x, y), w, wp, p);
 }
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }  // one pad word per 16 (bank spread)
@@ -96,13 +94,14 @@ __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }  // one pad w
 // g = B0 / (2d) + t, t < 2^st (B0 = global start of its 2D block), i.e. the
 // entries k = 2^(s0+st) + (B0 >> (log2 D + 1 - st)) + t.  They do not depend on
 // the data, so each pass loads all of them (2^r - 1 pairs) before touching smem.
+// Range discipline: every pass reduces on load and after its second stage, so no
+// value exceeds 0.5 p + 2 * 1.5 p < 4 p < 2^52.
 
 // local forward passes over a chunk (global position of element 0 = c0), stages with
 // distance chunk/2 .. 1; s0 = global stage index of the first local stage
 template <int LOGC>
-__device__ __forceinline__ void fwd_local(uint64_t* sm, int64_t c0, int s0, const uint64_t* w, const uint64_t* ws,
-                                          uint64_t p) {
-  constexpr int CH = 1 << LOGC;
+__device__ __forceinline__ void fwd_local(double* sm, int64_t c0, int s0, const double* w, const double* wp,
+                                          double p, double pinv) {
   int done = 0;
   // first pass takes LOGC % 4 stages (if any), the rest are radix-16
 #pragma unroll
@@ -112,9 +111,9 @@ __device__ __forceinline__ void fwd_local(uint64_t* sm, int64_t c0, int s0, cons
     const int D = 1 << logD;
     const int inner = D >> (r - 1);             // stride between the 2^r elements
     const int per = EPT >> r;                   // independent sub-butterflies per thread
-    uint64_t v[EPT];
+    double v[EPT];
     int base[EPT >> 1];
-    uint64_t tw[EPT >> 1][15], tws[EPT >> 1][15];
+    double tw[EPT >> 1][15], twp[EPT >> 1][15];
 #pragma unroll
     for (int h = 0; h < per; ++h) {
       const int id = threadIdx.x * per + h;
@@ -127,11 +126,11 @@ __device__ __forceinline__ void fwd_local(uint64_t* sm, int64_t c0, int s0, cons
 #pragma unroll
         for (int t = 0; t < (1 << st); ++t) {
           tw[h][(1 << st) - 1 + t] = __ldg(w + k0 + t);
-          tws[h][(1 << st) - 1 + t] = __ldg(ws + k0 + t);
+          twp[h][(1 << st) - 1 + t] = __ldg(wp + k0 + t);
         }
       }
 #pragma unroll
-      for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = sm[pad(base[h] + lo * inner)];
+      for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = red_d(sm[pad(base[h] + lo * inner)], p, pinv);
     }
 #pragma unroll
     for (int st = 0; st < r; ++st) {
@@ -142,8 +141,12 @@ __device__ __forceinline__ void fwd_local(uint64_t* sm, int64_t c0, int s0, cons
         for (int lo = 0; lo < (1 << r); ++lo) {
           if (lo & half) continue;
           const int t = (1 << st) - 1 + (lo >> (r - st));
-          ct_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], tws[h][t], p);
+          ct_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], twp[h][t], p);
         }
+      }
+      if (st == 1 && r > 2) {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) v[e] = red_d(v[e], p, pinv);
       }
     }
 #pragma unroll
@@ -157,8 +160,8 @@ __device__ __forceinline__ void fwd_local(uint64_t* sm, int64_t c0, int s0, cons
 
 // local inverse passes: stages with distance 1 .. chunk/2 (global stage index s0 + LOGC - 1 .. s0)
 template <int LOGC>
-__device__ __forceinline__ void inv_local(uint64_t* sm, int64_t c0, int s0, const uint64_t* w, const uint64_t* ws,
-                                          uint64_t p, uint64_t mu) {
+__device__ __forceinline__ void inv_local(double* sm, int64_t c0, int s0, const double* w, const double* wp,
+                                          double p, double pinv) {
   int done = 0;  // stages done, counted from distance 1 upwards
 #pragma unroll
   for (int pass = 0; pass < (LOGC + 3) / 4; ++pass) {
@@ -168,9 +171,9 @@ __device__ __forceinline__ void inv_local(uint64_t* sm, int64_t c0, int s0, cons
     const int D = 1 << logD;
     const int inner = Dmin;
     const int per = EPT >> r;
-    uint64_t v[EPT];
+    double v[EPT];
     int base[EPT >> 1];
-    uint64_t tw[EPT >> 1][15], tws[EPT >> 1][15];
+    double tw[EPT >> 1][15], twp[EPT >> 1][15];
 #pragma unroll
     for (int h = 0; h < per; ++h) {
       const int id = threadIdx.x * per + h;
@@ -185,11 +188,11 @@ __device__ __forceinline__ void inv_local(uint64_t* sm, int64_t c0, int s0, cons
 #pragma unroll
         for (int t = 0; t < (1 << u); ++t) {
           tw[h][(1 << u) - 1 + t] = __ldg(w + k0 + t);
-          tws[h][(1 << u) - 1 + t] = __ldg(ws + k0 + t);
+          twp[h][(1 << u) - 1 + t] = __ldg(wp + k0 + t);
         }
       }
 #pragma unroll
-      for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = sm[pad(base[h] + lo * inner)];
+      for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = red_d(sm[pad(base[h] + lo * inner)], p, pinv);
     }
 #pragma unroll
     for (int st = 0; st < r; ++st) {
@@ -201,47 +204,37 @@ __device__ __forceinline__ void inv_local(uint64_t* sm, int64_t c0, int s0, cons
         for (int lo = 0; lo < (1 << r); ++lo) {
           if (lo & half) continue;
           const int t = (1 << u) - 1 + (lo >> (st + 1));
-          // inputs of stage st are < 2^(st+1) p (sums double, Shoup outputs < 2p)
-          gs_bfly_lazy(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], tws[h][t], p,
-                       p << (st + 1));
+          gs_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], twp[h][t], p);
         }
+      }
+      if (st == 1 && r > 2) {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) v[e] = red_d(v[e], p, pinv);
       }
     }
 #pragma unroll
     for (int h = 0; h < per; ++h)
 #pragma unroll
-      for (int lo = 0; lo < (1 << r); ++lo)
-        sm[pad(base[h] + lo * inner)] = barrett2(v[h * (1 << r) + lo], p, mu);
+      for (int lo = 0; lo < (1 << r); ++lo) sm[pad(base[h] + lo * inner)] = v[h * (1 << r) + lo];
     __syncthreads();
     done += r;
   }
-}
-
-__device__ __forceinline__ uint64_t reduce4(uint64_t x, uint64_t p) {
-  if (x >= 2 * p) x -= 2 * p;
-  if (x >= p) x -= p;
-  return x;
-}
-// x < 2^63 -> x mod p, with mu = floor(2^64 / p)
-__device__ __forceinline__ uint64_t reduce_full(uint64_t x, uint64_t p, uint64_t mu) {
-  uint64_t r = x - __umul64hi(x, mu) * p;  // [0, 2p)
-  return r >= p ? r - p : r;
 }
 
 // grid: (batch * L) clusters of C CTAs; data (batch, L, N) u64
 template <int LOGN, int LOGCL>
 __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd_kernel(uint64_t* data, int L, Tables t) {
   constexpr int C = 1 << LOGCL, LOGC = LOGN - LOGCL, CH = 1 << LOGC, NT = CH / EPT;
-  extern __shared__ __align__(16) uint64_t sm[];
+  extern __shared__ __align__(16) double sm[];
   const int64_t poly = blockIdx.x / C;
   const int c = (int)(blockIdx.x % C);
   const int limb = (int)(poly % L);
-  const uint64_t p = t.p[limb];
-  const uint64_t* w = t.w + (size_t)limb * ((size_t)1 << LOGN);
-  const uint64_t* ws = t.ws + (size_t)limb * ((size_t)1 << LOGN);
+  const double p = (double)t.p[limb], pinv = 1.0 / p;
+  const double* w = t.w + (size_t)limb * ((size_t)1 << LOGN);
+  const double* wp = t.wp + (size_t)limb * ((size_t)1 << LOGN);
   uint64_t* x = data + poly * ((int64_t)1 << LOGN);
   if (C == 1) {
-    for (int i = threadIdx.x; i < CH; i += NT) sm[pad(i)] = x[i];
+    for (int i = threadIdx.x; i < CH; i += NT) sm[pad(i)] = (double)x[i];
     __syncthreads();
   } else {
     // cross-chunk stages 0 .. LOGCL-1: this CTA owns chunk offsets [c*CH/C, (c+1)*CH/C)
@@ -251,9 +244,9 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     bool waited = false;
     for (int o = c * (CH / C) + threadIdx.x; o < (c + 1) * (CH / C); o += NT) {
-      uint64_t v[C];
+      double v[C];
 #pragma unroll
-      for (int q = 0; q < C; ++q) v[q] = x[(int64_t)q * CH + o];
+      for (int q = 0; q < C; ++q) v[q] = (double)x[(int64_t)q * CH + o];
 #pragma unroll
       for (int s = 0; s < LOGCL; ++s) {
         const int half = C >> (s + 1);
@@ -262,7 +255,11 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd
           if (q & half) continue;
           const int g = q >> (LOGCL - s);
           const int k = (1 << s) + g;
-          ct_bfly(v[q], v[q + half], __ldg(w + k), __ldg(ws + k), p);
+          ct_bfly(v[q], v[q + half], __ldg(w + k), __ldg(wp + k), p);
+        }
+        if (s == 1) {
+#pragma unroll
+          for (int q = 0; q < C; ++q) v[q] = red_d(v[q], p, pinv);
         }
       }
       if (!waited) {
@@ -275,40 +272,41 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd
     if (!waited) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
     cluster.sync();
   }
-  fwd_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, ws, p);
+  fwd_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, wp, p, pinv);
   uint64_t* xo = x + (int64_t)c * CH;
-  const uint64_t mu = t.mu[limb];
-  for (int i = threadIdx.x; i < CH; i += NT) xo[i] = reduce_full(sm[pad(i)], p, mu);
+  for (int i = threadIdx.x; i < CH; i += NT) xo[i] = to_residue(sm[pad(i)], p, pinv);
 }
 
 template <int LOGN, int LOGCL>
 __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_inv_kernel(uint64_t* data, int L, Tables t) {
   constexpr int C = 1 << LOGCL, LOGC = LOGN - LOGCL, CH = 1 << LOGC, NT = CH / EPT;
-  extern __shared__ __align__(16) uint64_t sm[];
+  extern __shared__ __align__(16) double sm[];
   const int64_t poly = blockIdx.x / C;
   const int c = (int)(blockIdx.x % C);
   const int limb = (int)(poly % L);
-  const uint64_t p = t.p[limb];
-  const uint64_t* w = t.wi + (size_t)limb * ((size_t)1 << LOGN);
-  const uint64_t* ws = t.wis + (size_t)limb * ((size_t)1 << LOGN);
-  const uint64_t ninv = __ldg(w), ninvs = __ldg(ws);  // wi[0] = N^-1
+  const uint64_t pu = t.p[limb];
+  const double p = (double)pu, pinv = 1.0 / p;
+  const double* w = t.wi + (size_t)limb * ((size_t)1 << LOGN);
+  const double* wp = t.wip + (size_t)limb * ((size_t)1 << LOGN);
+  const double ninv = __ldg(w), ninvp = __ldg(wp);  // wi[0] = N^-1
   uint64_t* x = data + poly * ((int64_t)1 << LOGN);
   const uint64_t* xi = x + (int64_t)c * CH;
   for (int i = threadIdx.x; i < CH; i += NT) {
     const uint64_t v = xi[i];
-    sm[pad(i)] = v >= p ? v - p : v;  // tolerate inputs in [0, 2p)
+    sm[pad(i)] = (double)(v >= pu ? v - pu : v);  // tolerate inputs in [0, 2p)
   }
   __syncthreads();
-  inv_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, ws, p, t.mu[limb]);
+  inv_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, wp, p, pinv);
   if (C == 1) {
-    for (int i = threadIdx.x; i < CH; i += NT) x[i] = reduce4(shoup(sm[pad(i)], ninv, ninvs, p), p);
+    for (int i = threadIdx.x; i < CH; i += NT)
+      x[i] = to_residue(mulmod_d(red_d(sm[pad(i)], p, pinv), ninv, ninvp, p), p, pinv);
   } else {
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
     for (int o = c * (CH / C) + threadIdx.x; o < (c + 1) * (CH / C); o += NT) {
-      uint64_t v[C];
+      double v[C];
 #pragma unroll
-      for (int q = 0; q < C; ++q) v[q] = cluster.map_shared_rank(sm, q)[pad(o)];
+      for (int q = 0; q < C; ++q) v[q] = red_d(cluster.map_shared_rank(sm, q)[pad(o)], p, pinv);
 #pragma unroll
       for (int s = LOGCL - 1; s >= 0; --s) {
         const int half = C >> (s + 1);
@@ -317,11 +315,16 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_inv
           if (q & half) continue;
           const int g = q >> (LOGCL - s);
           const int k = (1 << s) + g;
-          gs_bfly(v[q], v[q + half], __ldg(w + k), __ldg(ws + k), p);
+          gs_bfly(v[q], v[q + half], __ldg(w + k), __ldg(wp + k), p);
+        }
+        if (s == LOGCL - 2) {
+#pragma unroll
+          for (int q = 0; q < C; ++q) v[q] = red_d(v[q], p, pinv);
         }
       }
 #pragma unroll
-      for (int q = 0; q < C; ++q) x[(int64_t)q * CH + o] = reduce4(shoup(v[q], ninv, ninvs, p), p);
+      for (int q = 0; q < C; ++q)
+        x[(int64_t)q * CH + o] = to_residue(mulmod_d(v[q], ninv, ninvp, p), p, pinv);
     }
     cluster.sync();  // peers may still read this CTA's chunk
   }
@@ -365,7 +368,6 @@ int brv(int x, int bits) {
   for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1) << (bits - 1 - i);
   return r;
 }
-uint64_t shoup_of(uint64_t w, uint64_t p) { return (uint64_t)(((unsigned __int128)w << 64) / p); }
 
 }  // namespace ntt
 }  // namespace sfhr
@@ -374,8 +376,9 @@ using namespace sfhr::ntt;
 
 struct sfhr_ntt_plan {
   int logn = 0, L = 0, device = 0;
-  std::vector<uint64_t> primes, w, ws, wi, wis;  // host copies
-  uint64_t* d_tab = nullptr;                     // [5][...] device copy
+  std::vector<uint64_t> primes, w, wi;   // host copies (integers)
+  std::vector<double> wd, wpd, wid, wipd;  // device tables: value and value / p
+  void* d_tab = nullptr;
   Tables t{};
 };
 
@@ -389,7 +392,7 @@ int nfail(int code, const std::string& m) {
 template <int LOGN, int LOGCL>
 cudaError_t launch_one(bool fwd, uint64_t* data, int64_t polys, int L, const Tables& t, cudaStream_t st) {
   constexpr int C = 1 << LOGCL, CH = 1 << (LOGN - LOGCL), NT = CH / EPT;
-  const size_t smem = (size_t)(CH + CH / 16) * 8;
+  const size_t smem = (size_t)(CH + CH / 16) * sizeof(double);
   auto kern = fwd ? ntt_fwd_kernel<LOGN, LOGCL> : ntt_inv_kernel<LOGN, LOGCL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -428,7 +431,7 @@ int sfhr_ntt_plan_create(int logn, int L, int prime_bits, int device, sfhr_ntt_p
   if (!out) return nfail(SFHR_EINVAL, "null output");
   if (logn < 10 || logn > 16) return nfail(SFHR_EINVAL, "log2 N must be in [10, 16]");
   if (L < 1 || L > 32) return nfail(SFHR_EINVAL, "limb count must be in [1, 32]");
-  // the lazy forward butterflies keep values below (2 log2 N + 1) p < 2^56 (see ct_bfly)
+  // the FP64 butterflies keep residues below 4p < 2^52 (see mulmod_d)
   if (prime_bits < 30 || prime_bits > 50) return nfail(SFHR_EINVAL, "prime bits must be in [30, 50]");
   auto* P = new sfhr_ntt_plan();
   P->logn = logn;
@@ -445,9 +448,11 @@ int sfhr_ntt_plan_create(int logn, int L, int prime_bits, int device, sfhr_ntt_p
     return nfail(SFHR_EINVAL, "not enough NTT primes");
   }
   P->w.assign(L * N, 0);
-  P->ws.assign(L * N, 0);
   P->wi.assign(L * N, 0);
-  P->wis.assign(L * N, 0);
+  P->wd.assign(L * N, 0);
+  P->wpd.assign(L * N, 0);
+  P->wid.assign(L * N, 0);
+  P->wipd.assign(L * N, 0);
   for (int i = 0; i < L; ++i) {
     const uint64_t p = P->primes[i];
     uint64_t psi = 0;  // primitive 2N-th root: psi^N = -1
@@ -466,36 +471,37 @@ int sfhr_ntt_plan_create(int logn, int L, int prime_bits, int device, sfhr_ntt_p
       const int e = brv((int)k, logn);
       const uint64_t a = pw[e], b = pwi[e];
       P->w[i * N + k] = a;
-      P->ws[i * N + k] = shoup_of(a, p);
       P->wi[i * N + k] = b;
-      P->wis[i * N + k] = shoup_of(b, p);
     }
     const uint64_t ninv = powmod(N % p, p - 2, p);
     P->wi[i * N] = ninv;  // slot 0 is unused by the butterflies
-    P->wis[i * N] = shoup_of(ninv, p);
+    for (uint64_t k = 0; k < N; ++k) {
+      P->wd[i * N + k] = (double)P->w[i * N + k];
+      P->wpd[i * N + k] = (double)P->w[i * N + k] / (double)p;
+      P->wid[i * N + k] = (double)P->wi[i * N + k];
+      P->wipd[i * N + k] = (double)P->wi[i * N + k] / (double)p;
+    }
   }
   if (device >= 0) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
-    const size_t words = (size_t)4 * L * N + 2 * L;
+    const size_t words = (size_t)4 * L * N + L;
     cudaError_t e = cudaMalloc(&P->d_tab, words * 8);
-    uint64_t* d = P->d_tab;
-    if (e == cudaSuccess) e = cudaMemcpy(d, P->w.data(), L * N * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d + L * N, P->ws.data(), L * N * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d + 2 * L * N, P->wi.data(), L * N * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d + 3 * L * N, P->wis.data(), L * N * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d + 4 * L * N, P->primes.data(), L * 8, cudaMemcpyHostToDevice);
-    std::vector<uint64_t> mus(L);
-    for (int i = 0; i < L; ++i) mus[i] = (uint64_t)(((unsigned __int128)1 << 64) / P->primes[i]);
-    if (e == cudaSuccess) e = cudaMemcpy(d + 4 * L * N + L, mus.data(), L * 8, cudaMemcpyHostToDevice);
+    double* d = static_cast<double*>(P->d_tab);
+    if (e == cudaSuccess) e = cudaMemcpy(d, P->wd.data(), L * N * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d + L * N, P->wpd.data(), L * N * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d + 2 * L * N, P->wid.data(), L * N * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d + 3 * L * N, P->wipd.data(), L * N * 8, cudaMemcpyHostToDevice);
+    uint64_t* dp = reinterpret_cast<uint64_t*>(d + 4 * L * N);
+    if (e == cudaSuccess) e = cudaMemcpy(dp, P->primes.data(), L * 8, cudaMemcpyHostToDevice);
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
       cudaFree(P->d_tab);
       delete P;
       return nfail(SFHR_ECUDA, std::string("ntt tables: ") + cudaGetErrorString(e));
     }
-    P->t = Tables{d, d + L * N, d + 2 * L * N, d + 3 * L * N, d + 4 * L * N, d + 4 * L * N + L};
+    P->t = Tables{d, d + L * N, d + 2 * L * N, d + 3 * L * N, dp};
   }
   *out = P;
   return SFHR_OK;
