@@ -177,6 +177,18 @@ int sfhr_ntt_forward(const sfhr_ntt_plan* plan, uint64_t* data, int64_t batch, v
 int sfhr_ntt_inverse(const sfhr_ntt_plan* plan, uint64_t* data, int64_t batch, void* stream);
 const char* sfhr_ntt_last_error(void);
 
+
+/* ---- device ciphertext-block wire codec (reference wire.py:99-124, 208-254) ----
+ * payload: DEVICE copy of a ROUND_REQ payload (4-byte aligned base, readable for 4
+ * bytes past its end); body_offsets: DEVICE (k,) byte offsets of each chunk's block
+ * body (after its 8-byte block header).  Writes out (k, npow, 2, N) u64 (lanes N..M-1 dropped) and
+ * sets *err (DEVICE int, caller-zeroed) to 1 when any lane, padding included, is >= 2^53
+ * (the reference's "torus numerator out of range"). */
+int sfhr_wire_unpack(const uint8_t* payload, const int64_t* body_offsets, int64_t k, int npow, int M, int N,
+                     uint64_t* out, int* err, void* stream);
+/* rows (count, 2, N) DEVICE -> body (count, 2, M) DEVICE, zero-padded lanes (encode_block body) */
+int sfhr_wire_pack(const uint64_t* rows, int64_t count, int M, int N, uint64_t* body, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,7 @@ INCLUDE = ROOT / "include"
 OBJ = PKG / "_build"
 LIB = PKG / "libsfhr_b200.so"
 
-SOURCES = ["keyswitch.cu", "ring_ops.cu", "linear_mma.cu", "ntt64.cu", "capi.cu", "plan.cpp", "perm.cpp"]
+SOURCES = ["keyswitch.cu", "ring_ops.cu", "linear_mma.cu", "ntt64.cu", "wire.cu", "capi.cu", "plan.cpp", "perm.cpp"]
 # (object name, source, extra -D flags): the stage-kernel template fan-out is
 # split into one translation unit per (t, l) so it compiles in parallel
 UNITS = [(s, s, []) for s in SOURCES] + [

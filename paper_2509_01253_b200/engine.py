@@ -271,7 +271,7 @@ class ServerEngine:
         out_map = None if rnd.final else self._perm(state, session_id, round_no, rnd.output_len)
         return in_map, out_map
 
-    def server_round(self, session_id: bytes, round_no: int, bundles: list):
+    def _check_round(self, session_id: bytes, round_no: int, n_chunks: int):
         state = self.sessions.get(session_id)
         if state is None:
             raise ProtocolError(ERR_BAD_SESSION, "unknown or expired session")
@@ -280,33 +280,79 @@ class ServerEngine:
         if not (1 <= round_no <= len(self.model.rounds)):
             raise ProtocolError(ERR_STALE_ROUND, "round beyond model depth")
         rnd = self.model.rounds[round_no - 1]
-        R = self.scheme.ring
+        k_expected = -(-rnd.input_len // self.scheme.ring.N)
+        if n_chunks != k_expected:
+            raise ProtocolError(ERR_MALFORMED, f"expected {k_expected} chunks, got {n_chunks}")
+        return state
+
+    def _run_round(self, state, session_id: bytes, round_no: int, power, exps):
         keys = self.clients[state.key_id]
-        k_expected = -(-rnd.input_len // R.N)
-        if len(bundles) != k_expected:
-            raise ProtocolError(ERR_MALFORMED, f"expected {k_expected} chunks, got {len(bundles)}")
-        power, exps = self._upload_bundles(bundles)
         in_map, out_map = self.round_maps(state, session_id, round_no)
         im = torch.from_numpy(in_map).to(self.dev, non_blocking=True)
         om = None if out_map is None else torch.from_numpy(out_map).to(self.dev, non_blocking=True)
         packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, im, om)
-        packs_host = to_host_u64(packs_dev)
-        packed = [packs_host[i] for i in range(packs_host.shape[0])]
         state.next_round += 1
         state.last_seen = time.monotonic()
         if round_no == len(self.model.rounds):
             self.sessions.pop(session_id, None)
+        self.total_key_switches += nks
+        return packs_dev, nks, times
+
+    def _stats(self, nks, times, n_chunks, n_packs):
+        return RoundStats(extract_s=times[0], linear_s=times[1], pack_s=times[2], key_switches=nks,
+                          packed_coefficients=n_packs * self.scheme.pack_factor,
+                          bytes_up=round_req_size(self.scheme, n_chunks),
+                          bytes_down=round_resp_size(self.scheme, n_packs))
+
+    def server_round(self, session_id: bytes, round_no: int, bundles: list):
+        """Reference ServerEngine.server_round (protocol.py:219-280): bundles in, packed cts out."""
+        state = self._check_round(session_id, round_no, len(bundles))
+        power, exps = self._upload_bundles(bundles)
+        packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps)
+        packs_host = to_host_u64(packs_dev)
+        packed = [packs_host[i] for i in range(packs_host.shape[0])]
         if self.extra_noise_std > 0:
             q = float(1 << 53)
             for pk in packed:
                 extra = np.rint(self._noise_rng.normal(0.0, self.extra_noise_std, pk.shape[-1]) * q)
                 pk[1] = (pk[1] + extra.astype(np.int64).astype(np.uint64)) & np.uint64((1 << 53) - 1)
-        self.total_key_switches += nks
-        st = RoundStats(extract_s=times[0], linear_s=times[1], pack_s=times[2], key_switches=nks,
-                        packed_coefficients=len(packed) * self.scheme.pack_factor,
-                        bytes_up=round_req_size(self.scheme, len(bundles)),
-                        bytes_down=round_resp_size(self.scheme, len(packed)))
-        return packed, st
+        return packed, self._stats(nks, times, len(bundles), len(packed))
+
+    def server_round_wire(self, session_id: bytes, round_no: int, payload) -> tuple:
+        """ROUND_REQ payload bytes -> (ROUND_RESP payload bytes, RoundStats).
+
+        The transport-facing form of server_round (reference ServerFrontend._round,
+        transport.py:82-89, decode_round_req -> server_round -> encode_round_resp):
+        the uploads are unpacked and range-checked on the GPU and the packed
+        outputs are encoded from device memory (wire.py:99-124, 208-254).
+        """
+        from .wire import WireError, decode_round_req_device, encode_round_resp_device
+        R = self.scheme.ring
+        try:
+            power, exps, gammas = decode_round_req_device(payload, R.N, self.dev)
+        except WireError as e:
+            raise ProtocolError(ERR_MALFORMED, e.reason) from e
+        state = self._check_round(session_id, round_no, int(power.shape[0]))
+        want = sorted(power_exponents(self.scheme.gamma, R))
+        if exps != want or any(g != self.scheme.gamma for g in gammas):
+            raise ProtocolError(ERR_MALFORMED, f"bundle exponents {exps} != required {want}")
+        if self.extra_noise_std > 0:
+            packed, st = self._round_from_device_with_noise(state, session_id, round_no, power, exps)
+            noisy = torch.from_numpy(np.stack(packed).view(np.int64)).to(self.dev)
+            return encode_round_resp_device(noisy, R.M, self.scheme.gamma), st
+        packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps)
+        resp = encode_round_resp_device(packs_dev, R.M, self.scheme.gamma)
+        return resp, self._stats(nks, times, int(power.shape[0]), int(packs_dev.shape[0]))
+
+    def _round_from_device_with_noise(self, state, session_id, round_no, power, exps):
+        packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps)
+        packs_host = to_host_u64(packs_dev)
+        packed = [packs_host[i] for i in range(packs_host.shape[0])]
+        q = float(1 << 53)
+        for pk in packed:
+            extra = np.rint(self._noise_rng.normal(0.0, self.extra_noise_std, pk.shape[-1]) * q)
+            pk[1] = (pk[1] + extra.astype(np.int64).astype(np.uint64)) & np.uint64((1 << 53) - 1)
+        return packed, self._stats(nks, times, int(power.shape[0]), len(packed))
 
     def round_device(self, round_no: int, key: DeviceKey, power, exps, in_map, out_map,
                      timed: bool = True, groups: Optional[tuple] = None, counter=None):
