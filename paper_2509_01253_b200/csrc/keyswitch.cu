@@ -299,13 +299,13 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst
 }
 
 template <int T, int A, int L, int PR>
-__device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem) {
+__device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& a, unsigned char* smem,
+                                          const int64_t row, const bool stage_twiddles) {
   const PrimeConst& pc = rc.pc[PR];
   const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
   const Geo<T, A> g(rc);
   const int N = g.N, n1 = g.n1, M = g.M;
   SmemLayout S = carve(smem, rc);
-  const int64_t row = blockIdx.x / rc.np;
   const uint64_t* xin = a.in + row * 2 * (int64_t)N;
   uint64_t* xout = a.out + row * 2 * (int64_t)N;
   cg::cluster_group cluster = cg::this_cluster();
@@ -322,7 +322,7 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
       nz |= (v.x | v.y | v.z | v.w) != 0;
     }
   }
-  {
+  if (stage_twiddles) {
     const uint4* wsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)PR * twid_stride(M));
     uint4* wdst = reinterpret_cast<uint4*>(S.wt);
     for (int k = threadIdx.x; k < twid_stride(M) / 4; k += blockDim.x) wdst[k] = wsrc[k];
@@ -515,6 +515,20 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   cluster.sync();
 }
 
+#ifndef SFHR_ROWS_PER_CLUSTER
+#define SFHR_ROWS_PER_CLUSTER 1
+#endif
+
+// a cluster processes SFHR_ROWS_PER_CLUSTER consecutive rows (twiddles staged once)
+template <int T, int A, int L, int PR>
+__device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem) {
+  const int64_t row0 = (int64_t)(blockIdx.x / rc.np) * SFHR_ROWS_PER_CLUSTER;
+  for (int rr = 0; rr < SFHR_ROWS_PER_CLUSTER; ++rr) {
+    if (row0 + rr >= a.B) break;  // uniform across the cluster
+    stage_row<T, A, L, PR>(rc, a, smem, row0 + rr, rr == 0);
+  }
+}
+
 #ifndef SFHR_T7_THREADS
 #define SFHR_T7_THREADS 384
 #endif
@@ -625,7 +639,7 @@ static cudaError_t launch_stage_tal(const RingConst& rc, const StageArgs& a, cud
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a.B * rc.np), 1, 1);
+  cfg.gridDim = dim3((unsigned)((a.B + SFHR_ROWS_PER_CLUSTER - 1) / SFHR_ROWS_PER_CLUSTER * rc.np), 1, 1);
   cfg.blockDim = dim3(stage_threads(rc), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -686,7 +700,8 @@ static cudaError_t launch_spec_t(const RingConst& rc, const SpecArgs& a, int njo
   const size_t smem = stage_smem_bytes(rc);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<njobs * rc.np, stage_threads(rc), smem, st>>>(rc, a);
+  const int nt = stage_threads(rc) < 512 ? stage_threads(rc) : 512;  // ks_spectra_kernel launch bound
+  kern<<<njobs * rc.np, nt, smem, st>>>(rc, a);
   return cudaGetLastError();
 }
 
