@@ -138,7 +138,7 @@ class _SessionState:
     key_id: bytes
     next_round: int = 1
     last_seen: float = field(default_factory=time.monotonic)
-    perms: object = None   # Future -> dict[(round, size)] -> np.ndarray
+    perms: object = None   # dict[(round, size)] -> Future[np.ndarray]
 
 
 @dataclass
@@ -181,7 +181,7 @@ class ServerEngine:
         self._bias_unit = to_dev(unit, self.dev)
         self._passes = [[DevicePass(p, self.dev) for p in lower_round(model, r)]
                         for r in range(len(model.rounds))]
-        self._perm_pool = ThreadPoolExecutor(max_workers=2)
+        self._perm_pool = ThreadPoolExecutor(max_workers=4)
         self.total_key_switches = 0
 
     # -- setup ---------------------------------------------------------------
@@ -198,18 +198,23 @@ class ServerEngine:
         return key_id
 
     def _perm_schedule(self, session_id: bytes) -> dict:
-        """All permutations a session will use, keyed by (round_no, size)."""
-        need = set()
+        """Futures of all permutations a session will use, keyed by (round_no, size).
+
+        Submitted in the order the rounds consume them, so round r waits only for
+        its own sigma_{r-1} / sigma_r while later ones are derived (C++, GIL released)
+        on the pool's other threads during the GPU work of the earlier rounds."""
+        need = []
         for r, rnd in enumerate(self.model.rounds, start=1):
             main = rnd.input_len - rnd.skip_len
-            need.add((r - 1, main))
+            need.append((r - 1, main))
             if rnd.skip_len:
-                need.add((rnd.skip_source + 1, rnd.skip_len))
+                need.append((rnd.skip_source + 1, rnd.skip_len))
             if not rnd.final:
-                need.add((r, rnd.output_len))
+                need.append((r, rnd.output_len))
         out = {}
-        for (rno, size) in sorted(need):
-            out[(rno, size)] = self._perm_now(session_id, rno, size)
+        for key in need:
+            if key not in out:
+                out[key] = self._perm_pool.submit(self._perm_now, session_id, *key)
         return out
 
     def _perm_now(self, session_id, round_no, size):
@@ -224,7 +229,7 @@ class ServerEngine:
         if session_id in self.sessions:
             raise ProtocolError(ERR_BAD_SESSION, "session id already in use")
         st = _SessionState(key_id=key_id)
-        st.perms = self._perm_pool.submit(self._perm_schedule, session_id)
+        st.perms = self._perm_schedule(session_id)
         self.sessions[session_id] = st
         return metadata_for(self.model, self.scheme)
 
@@ -234,9 +239,8 @@ class ServerEngine:
             del self.sessions[sid]
 
     def _perm(self, state: _SessionState, session_id: bytes, round_no: int, size: int) -> np.ndarray:
-        table = state.perms.result() if state.perms is not None else {}
-        p = table.get((round_no, size))
-        return p if p is not None else self._perm_now(session_id, round_no, size)
+        fut = state.perms.get((round_no, size)) if state.perms is not None else None
+        return fut.result() if fut is not None else self._perm_now(session_id, round_no, size)
 
     # -- round processing ------------------------------------------------------
 
@@ -270,6 +274,15 @@ class ServerEngine:
             in_map = np.concatenate([in_map, sk])
         out_map = None if rnd.final else self._perm(state, session_id, round_no, rnd.output_len)
         return in_map, out_map
+
+    def _to_host_pinned(self, t: torch.Tensor) -> np.ndarray:
+        """Device -> host through a grow-only pinned staging buffer (one DMA, one memcpy)."""
+        n = t.numel()
+        if getattr(self, "_pinned_out", None) is None or self._pinned_out.numel() < n:
+            self._pinned_out = torch.empty(max(n, 1 << 17), dtype=torch.int64, pin_memory=True)
+        stage = self._pinned_out[:n].view(t.shape)
+        stage.copy_(t)
+        return stage.numpy().view(np.uint64).copy()
 
     def _check_round(self, session_id: bytes, round_no: int, n_chunks: int):
         state = self.sessions.get(session_id)
@@ -309,7 +322,7 @@ class ServerEngine:
         state = self._check_round(session_id, round_no, len(bundles))
         power, exps = self._upload_bundles(bundles)
         packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps)
-        packs_host = to_host_u64(packs_dev)
+        packs_host = self._to_host_pinned(packs_dev)
         packed = [packs_host[i] for i in range(packs_host.shape[0])]
         if self.extra_noise_std > 0:
             q = float(1 << 53)
