@@ -65,7 +65,8 @@ __global__ void merge_kernel(const __grid_constant__ RingConst rc, const uint64_
 cudaError_t launch_merge(const RingConst& rc, const uint64_t* in, uint64_t* out, int64_t G,
                          int members, int rest, int stride, cudaStream_t st) {
   if (G == 0) return cudaSuccess;
-  dim3 grid((unsigned)(G * rest), (rc.N + 255) / 256, 2);
+  // ~4 coefficients per thread: more independent gathers in flight, fewer tiny blocks
+  dim3 grid((unsigned)(G * rest), (rc.N + 1023) / 1024, 2);
   merge_kernel<<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride);
   return cudaGetLastError();
 }
