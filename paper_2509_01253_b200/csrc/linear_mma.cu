@@ -31,7 +31,10 @@ namespace sfhr {
 namespace {
 
 constexpr int EPI_WARPS = 4;              // TMEM lanes 0-127
-constexpr int PRODUCERS = 128;            // cp.async gather threads
+#ifndef SFHR_MMA_PRODUCERS
+#define SFHR_MMA_PRODUCERS 128
+#endif
+constexpr int PRODUCERS = SFHR_MMA_PRODUCERS;  // cp.async gather threads
 constexpr int MMA_THREADS = EPI_WARPS * 32 + PRODUCERS + 32;
 constexpr int KC = 64;                    // taps per pipeline stage (2 MMAs)
 constexpr int NSTAGE = 4;
@@ -239,12 +242,13 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
           const uint32_t bdst = ring + stage * SB + STAGE_BYTES;
           for (int i = pt; i < nkb * (Np / 8) * 8; i += PRODUCERS) cp16(bdst + 16 * i, bsrc + 16 * i, 16);
         }
+        constexpr int TSTRIDE = PRODUCERS / 8;  // taps covered by one sweep of the producers
 #pragma unroll
-        for (int i = 0; i < KC / 16; ++i) {
-          const int tap = tb + 16 * i;
+        for (int i = 0; i < KC / TSTRIDE; ++i) {
+          const int tap = tb + TSTRIDE * i;
           if (tap < ntaps) {
             const unsigned char* rp = cp[tap];
-            cp16(dst + i * 16 * 128, rp ? rp + off : in8, rp ? nbytes : 0u);
+            cp16(dst + i * TSTRIDE * 128, rp ? rp + off : in8, rp ? nbytes : 0u);
           }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(full0 + 8 * stage)
