@@ -128,6 +128,9 @@ typedef struct {
   const int32_t* mma_rows;   /* canonical output row of each tile row */
   const uint8_t* mma_w;      /* packed s8 weights, UMMA K-major no-swizzle core matrices */
   int32_t mma_max_np, mma_max_kp;  /* largest N_pad / K_pad over the tiles */
+  /* Row counts of `in` / `round_in`; when given (> 0) the tensor-core tiles gather their
+   * taps with TMA (tile::gather4 over a 2-D tensor map) instead of per-thread cp.async. */
+  int64_t in_rows, round_in_rows;
 } sfhr_linear_desc;
 int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* desc, void* stream);
 /* sizeof(sfhr_linear_desc), for binding-layout checks */

@@ -102,7 +102,8 @@ class LinearDesc(C.Structure):
                [("lanes", C.c_int64), ("body_off", C.c_int64)] + \
                [("mma_tiles", C.c_void_p), ("n_mma_tiles", C.c_int64)] + \
                [(n, C.c_void_p) for n in ("mma_cols", "mma_rows", "mma_w")] + \
-               [("mma_max_np", C.c_int32), ("mma_max_kp", C.c_int32)]
+               [("mma_max_np", C.c_int32), ("mma_max_kp", C.c_int32)] + \
+               [("in_rows", C.c_int64), ("round_in_rows", C.c_int64)]
 
 
 # -- mirrors of the device constant block (debug / CPU verification only) --

@@ -79,6 +79,32 @@ struct DeviceGuard {
   }
 };
 
+// 2-D TMA map over (rows, lanes) u64 rows: box = 16 lanes x 1 row, 128B swizzle (the UMMA A layout),
+// out-of-bounds rows / lanes zero-filled.  cuTensorMapEncodeTiled comes from the driver entry point.
+bool make_row_map(CUtensorMap* m, const void* base, int64_t rows, int64_t lanes) {
+  using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                          CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<Fn>(p);
+  }
+  if (!fn || !base || rows <= 0 || rows > 0x7ffffffe || lanes <= 0) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)lanes, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)lanes * 8};
+  const cuuint32_t box[2] = {16, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int key_slot(const sfhr_key* key, uint32_t d) {
   const uint32_t M = (uint32_t)key->ctx->plan.rc.M;
   auto it = key->slot.find(d % M);
@@ -417,6 +443,7 @@ int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* d, void* stream) {
     if (!d->mma_tiles || !d->mma_cols || !d->mma_rows || !d->mma_w)
       return fail(SFHR_EINVAL, "incomplete tensor-core tile description");
     LinearMmaArgs m;
+    std::memset(&m, 0, sizeof(m));
     m.in = a.in;
     m.in_map = a.in_map;
     m.round_in = a.round_in;
@@ -439,6 +466,15 @@ int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* d, void* stream) {
     per = per < 1 ? 1 : (per > 16 ? 16 : per);
     const int64_t chunks = (n_mt + per - 1) / per;
     m.mt_per_cta = (int)((n_mt + chunks - 1) / chunks);
+    m.in_rows = d->in_rows;
+    m.rin_rows = d->round_in_rows;
+    m.use_tma = 0;
+    if (d->in_rows > 0 && a.lanes % 2 == 0) {
+      const bool rin_ok = d->round_in_rows > 0 && a.round_in;
+      if (make_row_map(&m.tm_in, a.in, d->in_rows, a.lanes) &&
+          make_row_map(&m.tm_rin, rin_ok ? a.round_in : a.in, rin_ok ? d->round_in_rows : d->in_rows, a.lanes))
+        m.use_tma = 1;
+    }
     CK(launch_linear_mma(m, d->mma_max_np, d->mma_max_kp, (cudaStream_t)stream), "linear tensor-core kernel");
     ++g_launches;
   }

@@ -113,6 +113,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 
 __device__ __forceinline__ uint64_t sx(int v) { return (uint64_t)(int64_t)v; }
 
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+// four rows (r0..r3) x 16 u64 lanes from column c0 of a 2-D TMA map, 128B-swizzled, into 4 x 128 B
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, int c0, int r0, int r1, int r2,
+                                            int r3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 }  // namespace
 
 // byte offsets of the dynamic shared-memory carve-up (host and device agree)
@@ -175,7 +193,15 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   cp_commit();
   const unsigned char* in8 = reinterpret_cast<const unsigned char*>(a.in);
   const unsigned char* rin8 = reinterpret_cast<const unsigned char*>(a.round_in);
-  for (int k = tid; k < Kp; k += MMA_THREADS) {
+  int2* trow = reinterpret_cast<int2*>(sm + L.colp);  // TMA mode: (row, map) per tap, same slot
+  for (int k = tid; k < Kp && a.use_tma; k += MMA_THREADS) {
+    const int col = a.tcols[c0 + k];
+    int2 e = make_int2(0x7fffffff, 0);  // zero tap: out-of-bounds row, zero-filled by the TMA
+    if (col >= 0) e = make_int2((int)(a.in_map ? a.in_map[col] : (int64_t)col), 0);
+    else if (col <= -2) e = make_int2((int)(a.round_map ? a.round_map[-(col + 2)] : (int64_t)(-(col + 2))), 1);
+    trow[k] = e;
+  }
+  for (int k = tid; k < Kp && !a.use_tma; k += MMA_THREADS) {
     const int col = a.tcols[c0 + k];
     const unsigned char* p = nullptr;
     if (col >= 0) {
@@ -198,7 +224,7 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   }
   if (tid == 0) {
     for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(full0 + 8 * i, PRODUCERS);
+      mbar_init(full0 + 8 * i, a.use_tma ? 1 : PRODUCERS);
       mbar_init(empty0 + 8 * i, 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -221,7 +247,37 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   const uint32_t tmem = *tslot;
   const int nkc = (Kp + KC - 1) / KC;
 
-  if (warp >= EPI_WARPS && warp < EPI_WARPS + PRODUCERS / 32) {
+  if (a.use_tma && warp == EPI_WARPS) {
+    // ---------------- TMA producer warp: tile::gather4 per 4 taps, spread over the lanes ----------------
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int mt = mt0; mt < mt1; ++mt) {
+      for (int kc = 0; kc < nkc; ++kc) {
+        mbar_wait(empty0 + 8 * stage, phase ^ 1);
+        const int ntaps = min(KC, Kp - kc * KC);  // multiple of 32
+        const int nkb = ntaps / 16;
+        const uint32_t bbytes = L.stream ? (uint32_t)(nkb * (Np / 8) * 128) : 0u;
+        const uint32_t full = full0 + 8 * stage;
+        if (lane == 0) mbar_expect_tx(full, (uint32_t)ntaps * 128u + bbytes);
+        __syncwarp();
+        const uint32_t dst = ring + stage * SB;
+        const int2* tr = trow + kc * KC;
+        const int g = 4 * lane;  // <= 16 lanes active (KC = 64 taps)
+        if (g < ntaps) {
+          // a group of 4 taps never mixes the two inputs (host pads the pass-input taps to 4)
+          const int2 e0 = tr[g], e1 = tr[g + 1], e2 = tr[g + 2], e3 = tr[g + 3];
+          const int which = e0.y | e1.y | e2.y | e3.y;
+          tma_gather4(dst + g * 128, which ? &a.tm_rin : &a.tm_in, mt * 16, e0.x, e1.x, e2.x, e3.x, full);
+        }
+        if (L.stream && lane == 31)
+          bulk_copy(dst + STAGE_BYTES, wsrc + (size_t)kc * (KC / 16) * (Np / 8) * 128, bbytes, full);
+        if (++stage == NSTAGE) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (!a.use_tma && warp >= EPI_WARPS && warp < EPI_WARPS + PRODUCERS / 32) {
     // ---------------- producers ----------------
     const int pt = tid - EPI_WARPS * 32;
     const int c = pt & 7, tb = pt >> 3;          // 16-byte chunk, first tap (taps tb + 16 i)

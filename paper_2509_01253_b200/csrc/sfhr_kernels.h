@@ -2,6 +2,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "sfhr_common.cuh"
@@ -78,6 +79,10 @@ cudaError_t launch_linear(const RingConst& rc, const LinearArgs& a, cudaStream_t
 
 // tensor-core (tcgen05 kind::i8) variant over tile groups (linear_mma.cu)
 struct LinearMmaArgs {
+  CUtensorMap tm_in;         // TMA maps over the pass input / round input rows (use_tma)
+  CUtensorMap tm_rin;
+  int use_tma;               // 1: taps gathered by tile::gather4 TMA (rows known), 0: cp.async
+  int64_t in_rows, rin_rows;
   const uint64_t* in;
   const int64_t* in_map;
   const uint64_t* round_in;

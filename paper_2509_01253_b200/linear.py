@@ -24,6 +24,9 @@ _LIMB = 18
 MMA_MAX_ROWS = 256      # N of one tcgen05 tile group
 MMA_MAX_KPAD = 8192     # taps per tile group (row-pointer table in shared memory)
 MMA_ENABLED = os.environ.get("SFHR_LINEAR_MMA", "1") != "0"
+# tile::gather4 TMA producer instead of per-thread cp.async gathers (A/B on B200: 153.5 vs 151.1 ms
+# per ResNet-20 inference, so cp.async stays the default)
+MMA_TMA = os.environ.get("SFHR_LINEAR_TMA", "0") == "1"
 
 
 @dataclass
@@ -95,7 +98,8 @@ def split_mma_tiles(ps: LinearPass):
                 ex_vals = np.zeros((tot, len(ex_cols)), np.int64)
                 for ri, (a, b) in enumerate(zip(lo, hi)):
                     np.add.at(ex_vals[ri], np.searchsorted(ex_cols, ps.ex_col[a:b]), ps.ex_w[a:b])
-        kk = nc + len(ex_cols)
+        nc4 = (nc + 3) // 4 * 4 if len(ex_cols) else nc  # TMA gathers 4 taps of one input at a time
+        kk = nc4 + len(ex_cols)
         k_pad = (kk + 31) // 32 * 32
         n_pad = (tot + 15) // 16 * 16
         key = tuple(int(g[q][2]) for q in run) + tuple(int(g[q][4]) for q in run)
@@ -107,7 +111,7 @@ def split_mma_tiles(ps: LinearPass):
             wt = np.concatenate([wv[int(g[q][2]):int(g[q][2]) + nc * ROWS_PER_GROUP]
                                  .reshape(nc, ROWS_PER_GROUP)[:, :int(g[q][4])].T for q in run])
             if ex_vals is not None:
-                wt = np.concatenate([wt, ex_vals], axis=1)
+                wt = np.concatenate([wt, np.zeros((tot, nc4 - nc), np.int64), ex_vals], axis=1)
             if np.abs(wt).max(initial=0) > 127 or k_pad > MMA_MAX_KPAD or len(ex_cols) > 256:
                 rest.extend(run)
                 i = j
@@ -126,7 +130,7 @@ def split_mma_tiles(ps: LinearPass):
         tiles.append((ncols, k_pad, woff, nrows, tot, n_pad, 0, 0))
         tc = np.full(k_pad, -1, np.int64)
         tc[:nc] = cols
-        tc[nc:kk] = -(ex_cols + 2)
+        tc[nc4:kk] = -(ex_cols + 2)
         tcols.append(tc)
         ncols += k_pad
         trows.append(rows_run)
@@ -188,6 +192,9 @@ def run_pass(ctx: RingContext, p: DevicePass, inp, in_map, round_in, round_map, 
     d.mma_tiles, d.n_mma_tiles = nat.ptr(p.mma_tiles), p.n_mma_tiles
     d.mma_cols, d.mma_rows, d.mma_w = nat.ptr(p.mma_cols), nat.ptr(p.mma_rows), nat.ptr(p.mma_w)
     d.mma_max_np, d.mma_max_kp = p.mma_max_np, p.mma_max_kp
+    if MMA_TMA and p.n_mma_tiles:
+        d.in_rows = int(inp.shape[0])
+        d.round_in_rows = int(round_in.shape[0]) if round_in is not None else 0
     import ctypes as C
     nat.check(nat.lib.sfhr_linear_pass(ctx.h, C.byref(d), ctx.stream()))
 

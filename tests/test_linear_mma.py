@@ -143,12 +143,13 @@ def test_mma_round_matches_cuda_core_kernel(net, r, monkeypatch):
     if r == 1:  # exercise the bias path as well
         passes[-1].bias = rng.integers(-5, 6, passes[-1].out_len)
     outs = []
-    for enabled in (True, False):
+    for enabled, tma in ((True, False), (True, True), (False, False)):
         monkeypatch.setattr(lin, "MMA_ENABLED", enabled)
+        monkeypatch.setattr(lin, "MMA_TMA", tma)
         dps = [lin.DevicePass(p, ctx.dev) for p in passes]
         assert any(dp.n_mma_tiles > 0 for dp in dps) == enabled
         out = torch.zeros((rnd.output_len, 2, R.N), dtype=torch.int64, device=ctx.dev)
         lin.run_round(ctx, dps, x, in_map, out, out_map, unit)
         torch.cuda.synchronize()
         outs.append(out.cpu().numpy())
-    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[2])
