@@ -367,6 +367,7 @@ int sfhr_keyswitch_batch(sfhr_ctx* ctx, const sfhr_key* key, uint32_t d, const u
                          int64_t B, int skip_zero, unsigned long long* counter, void* stream) {
   if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
   if (!ctx || !key) return fail(SFHR_EINVAL, "null argument");
+  if (B == 0) return SFHR_OK;
   if (in == out) return fail(SFHR_EINVAL, "in and out must not alias");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g(ctx->device);
@@ -378,6 +379,7 @@ int sfhr_stage_batch(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, i
                      uint64_t* out, int64_t B, int skip_zero, unsigned long long* counter, void* stream) {
   if (ctx && ctx->device < 0) return fail(SFHR_EINVAL, "planning-only context (device -1) cannot compute");
   if (!ctx || !key || !reps || nreps < 1) return fail(SFHR_EINVAL, "bad argument");
+  if (B == 0) return SFHR_OK;
   if (in == out) return fail(SFHR_EINVAL, "in and out must not alias");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g(ctx->device);

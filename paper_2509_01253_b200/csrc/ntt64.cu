@@ -529,7 +529,9 @@ int sfhr_ntt_plan_tables(const sfhr_ntt_plan* P, uint64_t* w, uint64_t* wi) {
 }
 
 static int ntt_run(bool fwd, const sfhr_ntt_plan* P, uint64_t* data, int64_t batch, void* stream) {
-  if (!P || !data) return nfail(SFHR_EINVAL, "null argument");
+  if (!P) return nfail(SFHR_EINVAL, "null plan");
+  if (batch == 0) return SFHR_OK;  // an empty batch may come with a null data pointer
+  if (!data) return nfail(SFHR_EINVAL, "null data");
   if (P->device < 0) return nfail(SFHR_EINVAL, "planning-only NTT plan (device -1) cannot compute");
   if (batch < 0) return nfail(SFHR_EINVAL, "negative batch");
   if (batch == 0) return SFHR_OK;

@@ -1,0 +1,103 @@
+"""GPU edge cases: empty and ragged batches, all-zero rows and the skip_zero
+KS counting (reference tracepack.py:268-285, 299-303), extraction at 1 and N
+rows, missing key indices, and the RNS NTT on an empty batch.  Bit-exact
+against the oracle wherever there is an output."""
+
+import numpy as np
+import pytest
+
+from conftest import has_cuda, u53
+from oracle import keyswitch as oks
+from oracle import pack as opk
+from oracle import protocol as opr
+from oracle import scheme as osc
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")]
+
+
+def _engine(b, gamma, seed=3):
+    from paper_2509_01253_b200.keyswitch import KeySwitchEngine, KeySwitchKeySet
+    from paper_2509_01253_b200.params import GadgetParams, RingParams
+    sch = osc.preset(b, gamma)
+    ksk = opr.OracleClient(sch, seed=seed).make_ksk()
+    R = RingParams(sch.ring.t, sch.ring.alpha, sch.ring.p_bits)
+    g = GadgetParams(sch.gadget.D, sch.gadget.l)
+    eng = KeySwitchEngine(KeySwitchKeySet(ksk.keys, g, ksk.delta, R), gamma=gamma)
+    return sch, ksk, eng
+
+
+@pytest.mark.parametrize("b", [8, 12, 16])
+def test_empty_batches(b):
+    sch, ksk, eng = _engine(b, 1)
+    N = sch.ring.N
+    d = sorted(ksk.keys)[0]
+    empty = np.zeros((0, 2, N), np.uint64)
+    assert eng.switch_batch(empty, d).shape == (0, 2, N)
+    assert eng.automorphism_batch(empty, d).shape == (0, 2, N)
+    assert eng.stage_batch(empty, [1, d]).shape == (0, 2, N)
+
+
+@pytest.mark.parametrize("b,gamma", [(8, 0), (12, 1), (16, 2)])
+def test_zero_rows_skip_zero_counting(b, gamma):
+    """Zero rows switch to zero and are not counted with skip_zero (the padding of the
+    last pack group); counted otherwise.  Ragged batch sizes (1, 7, 130)."""
+    from paper_2509_01253_b200.tracepack import KsCounter
+    sch, ksk, eng = _engine(b, gamma)
+    ref = oks.KsEngine(ksk, "exact")
+    R = sch.ring
+    reps = opk.stage_reps_above(R.alpha - 1, R)
+    for B in (1, 7, 130):
+        x = u53(B, (B, 2, R.N))
+        x[::3] = 0
+        live = int(np.any(x.reshape(B, -1) != 0, axis=1).sum())
+        for skip in (True, False):
+            c = KsCounter()
+            got = eng.stage_batch(x, reps, counter=c, skip_zero=skip)
+            assert c.total_key_switches == (live if skip else B) * (len(reps) - 1)
+            assert np.all(got[::3] == 0)
+        if B <= 7:  # exact oracle is slow: check the values on the small batches
+            assert np.array_equal(got, opk.apply_stage(x, reps, ref, None, False))
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_extract_one_and_full_chunk(b):
+    from paper_2509_01253_b200.params import RingParams
+    from paper_2509_01253_b200.tracepack import PowerBundle, partial_extract, power_exponents
+    from paper_2509_01253_b200.keyswitch import RlweCiphertext
+    sch = osc.preset(b, 1)
+    R = sch.ring
+    Rm = RingParams(R.t, R.alpha, R.p_bits)
+    exps = power_exponents(1, Rm)
+    power = u53(77, (len(exps), 2, R.N))
+    bundle = PowerBundle(1, {d: RlweCiphertext(power[q, 0], power[q, 1]) for q, d in enumerate(exps)})
+    obundle = opk.Bundle(1, {d: oks.Ct(power[q, 0], power[q, 1]) for q, d in enumerate(exps)})
+    full = partial_extract(bundle, None, R.N, Rm)
+    one = partial_extract(bundle, None, 1, Rm)
+    assert one.shape == (1, 2, R.N) and np.array_equal(one[0], full[0])
+    assert np.array_equal(full, opk.extract(obundle, R.N, R))
+    with pytest.raises(ValueError):
+        partial_extract(bundle, None, R.N + 1, Rm)
+
+
+def test_missing_key_index_raises():
+    sch, ksk, eng = _engine(12, 1)
+    N = sch.ring.N
+    bad = max(ksk.keys) + 1
+    while bad in ksk.keys:
+        bad += 1
+    with pytest.raises(KeyError):
+        eng.switch_batch(np.zeros((2, 2, N), np.uint64), bad)
+    with pytest.raises(KeyError):
+        eng.stage_batch(np.zeros((2, 2, N), np.uint64), [1, bad])
+
+
+def test_ntt_empty_batch_and_bad_shapes():
+    import torch
+    from paper_2509_01253_b200.ntt import RnsNtt
+    pl = RnsNtt(12, 2, 50, device=0)
+    x = torch.zeros((0, 2, 1 << 12), dtype=torch.int64, device="cuda")
+    assert pl.forward(x).shape == (0, 2, 1 << 12)
+    with pytest.raises(ValueError):
+        pl.forward(torch.zeros((1, 3, 1 << 12), dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError):
+        pl.forward(torch.zeros((1, 2, 1 << 12), dtype=torch.int32, device="cuda"))
