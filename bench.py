@@ -344,6 +344,13 @@ def stage_traffic(N):
     alg = [l["launch__grid_size"] / 3 * 32 * 2058 for l in launches]
     out = {"traffic": sum(tr) / len(tr), "unit": "bytes per launch", "launches": len(tr),
            "algorithmic_bytes_per_launch": sum(alg) / len(alg), "source": f"profiles/{f.name}"}
+    # the compute side of the same capture: this kernel is issue/latency bound, not HBM bound
+    def mean(key):
+        v = [l.get(key) for l in launches if isinstance(l.get(key), float)]
+        return sum(v) / len(v) / 100.0 if v else None
+    out["sm_issue_active_frac"] = mean("smsp__issue_active.avg.pct_of_peak_sustained_active")
+    out["fma_pipe_frac"] = mean("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active")
+    out["alu_pipe_frac"] = mean("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active")
     if N == 2058:
         out["traffic_over_algorithmic"] = sum(tr) / sum(alg)
     return out

@@ -86,15 +86,14 @@ bool make_row_map(CUtensorMap* m, const void* base, int64_t rows, int64_t lanes)
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
   static Fn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;
+  std::call_once(once, [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<Fn>(p);
-  }
+  });
   if (!fn || !base || rows <= 0 || rows > 0x7ffffffe || lanes <= 0) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)lanes, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)lanes * 8};
