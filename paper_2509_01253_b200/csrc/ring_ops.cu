@@ -37,6 +37,7 @@ cudaError_t launch_automorphism(const RingConst& rc, uint32_t dinv, const uint64
 // ---------------------------------------------------------------------------
 // tower merge (reference tracepack.py:307-316 with ring.py:77-84)
 
+template <int MEM>
 __global__ void merge_kernel(const __grid_constant__ RingConst rc, const uint64_t* __restrict__ in,
                              uint64_t* __restrict__ out, int members, int rest, int stride) {
   const int64_t orow = blockIdx.x;          // (g, r)
@@ -44,19 +45,38 @@ __global__ void merge_kernel(const __grid_constant__ RingConst rc, const uint64_
   const int64_t g = orow / rest;
   const int r = (int)(orow - g * rest);
   const int N = rc.N, M = rc.M;
+  const int nm = MEM ? MEM : members;
   for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < N; k += gridDim.y * blockDim.x) {
     const int km = (int)fastmod((uint32_t)k, rc.n1, rc.magicN1);
+    uint64_t t1[MEM ? MEM : 1], t2[MEM ? MEM : 1];
     uint64_t acc = 0;
-    for (int a = 0; a < members; ++a) {
-      const uint64_t* v = in + ((g * members + a) * (int64_t)rest + r) * 2 * N + (int64_t)comp * N;
+    // all members' loads are issued before any is consumed (MEM is the compile-time count)
+#pragma unroll
+    for (int a = 0; a < (MEM ? MEM : 1); ++a) {
+      const uint64_t* v = in + ((g * nm + a) * (int64_t)rest + r) * 2 * N + (int64_t)comp * N;
       const int e = (int)(((int64_t)a * stride) % M);
       int s1 = k - e;
       if (s1 < 0) s1 += M;
       int s2 = N + km - e;
       if (s2 < 0) s2 += M;
-      uint64_t t = s1 < N ? v[s1] : 0ull;
-      if (s2 < N) t -= v[s2];
-      acc += t;
+      t1[a] = s1 < N ? v[s1] : 0ull;
+      t2[a] = s2 < N ? v[s2] : 0ull;
+    }
+    if (MEM) {
+#pragma unroll
+      for (int a = 0; a < (MEM ? MEM : 1); ++a) acc += t1[a] - t2[a];
+    } else {
+      for (int a = 0; a < nm; ++a) {
+        const uint64_t* v = in + ((g * nm + a) * (int64_t)rest + r) * 2 * N + (int64_t)comp * N;
+        const int e = (int)(((int64_t)a * stride) % M);
+        int s1 = k - e;
+        if (s1 < 0) s1 += M;
+        int s2 = N + km - e;
+        if (s2 < 0) s2 += M;
+        uint64_t t = s1 < N ? v[s1] : 0ull;
+        if (s2 < N) t -= v[s2];
+        acc += t;
+      }
     }
     out[orow * 2 * N + (int64_t)comp * N + k] = acc & QMASK;
   }
@@ -65,9 +85,16 @@ __global__ void merge_kernel(const __grid_constant__ RingConst rc, const uint64_
 cudaError_t launch_merge(const RingConst& rc, const uint64_t* in, uint64_t* out, int64_t G,
                          int members, int rest, int stride, cudaStream_t st) {
   if (G == 0) return cudaSuccess;
-  // ~4 coefficients per thread: more independent gathers in flight, fewer tiny blocks
-  dim3 grid((unsigned)(G * rest), (rc.N + 1023) / 1024, 2);
-  merge_kernel<<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride);
+  dim3 grid((unsigned)(G * rest), (rc.N + 255) / 256, 2);
+  switch (members) {  // t - 1 or t members: 2..7 for the production rings
+    case 2: merge_kernel<2><<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride); break;
+    case 3: merge_kernel<3><<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride); break;
+    case 4: merge_kernel<4><<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride); break;
+    case 5: merge_kernel<5><<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride); break;
+    case 6: merge_kernel<6><<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride); break;
+    case 7: merge_kernel<7><<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride); break;
+    default: merge_kernel<0><<<grid, 256, 0, st>>>(rc, in, out, members, rest, stride); break;
+  }
   return cudaGetLastError();
 }
 
