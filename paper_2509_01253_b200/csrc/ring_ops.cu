@@ -166,27 +166,25 @@ __global__ void __launch_bounds__(EX_THREADS) extract_tiled_kernel(const __grid_
     ssh[r][q] = fastmod((uint32_t)(a.cvec[i0 + r] * n1) * d, M, rc.magicM);
   }
   __syncthreads();
-  for (int r = 0; r < nrows; ++r) {
-    uint64_t* dst = a.rows + (g0 + r) * 2 * N;
-    for (int lane = threadIdx.x; lane < 2 * N; lane += EX_THREADS) {
-      const int comp = lane >= N;
-      const int k = lane - comp * N;
-      const uint32_t km = fastmod((uint32_t)k, n1, rc.magicN1);
+  // lanes outer (their component / fold offsets are row-invariant), rows inner
+  for (int lane = threadIdx.x; lane < 2 * N; lane += EX_THREADS) {
+    const int comp = lane >= N;
+    const uint32_t k = (uint32_t)(lane - comp * N);
+    const uint32_t kf = (uint32_t)N + fastmod(k, n1, rc.magicN1);  // folded position N + (k mod n1)
+    uint64_t* dst = a.rows + g0 * 2 * N + lane;
+    for (int r = 0; r < nrows; ++r) {
       uint64_t acc = 0;
       for (int q = 0; q < np; ++q) {
         const uint64_t* ct = sp + (2 * q + comp) * M;
         const uint32_t id = sid[r][q], sh = ssh[r][q];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t x = id + (h ? (uint32_t)(N + km) : (uint32_t)k);
-          x = x >= (uint32_t)M ? x - M : x;
-          x = x >= (uint32_t)M ? x - M : x;
-          const uint32_t y = x >= sh ? x - sh : x + M - sh;
-          const uint64_t t = ct[x] - ct[y];
-          acc = h ? acc - t : acc + t;
-        }
+        uint32_t x0 = id + k, x1 = id + kf;  // both < 2M
+        x0 = x0 >= (uint32_t)M ? x0 - M : x0;
+        x1 = x1 >= (uint32_t)M ? x1 - M : x1;
+        const uint32_t y0 = x0 >= sh ? x0 - sh : x0 + M - sh;
+        const uint32_t y1 = x1 >= sh ? x1 - sh : x1 + M - sh;
+        acc += (ct[x0] - ct[y0]) - (ct[x1] - ct[y1]);
       }
-      dst[lane] = (acc * a.cu) & QMASK;
+      dst[(int64_t)r * 2 * N] = (acc * a.cu) & QMASK;
     }
   }
 }
