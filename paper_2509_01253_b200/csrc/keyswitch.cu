@@ -289,10 +289,17 @@ struct SmemLayout {
   uint32_t* buf;  // (nb, N) transform buffers
 };
 
+// the mask buffer doubles as the CRT receive buffer [np][2][per] u32 (per = ceil(N / np))
+__host__ __device__ __forceinline__ size_t xa_region_bytes(const RingConst& rc) {
+  const size_t per = (size_t)(rc.N + rc.np - 1) / rc.np;
+  const size_t recv = (size_t)rc.np * 2 * per * 4, mask = (size_t)rc.N * 8;
+  return ((recv > mask ? recv : mask) + 15) & ~(size_t)15;
+}
+
 __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst& rc) {
   SmemLayout s;
   s.xa = reinterpret_cast<uint64_t*>(smem);
-  s.wt = reinterpret_cast<uint32_t*>(smem + (size_t)rc.N * 8);
+  s.wt = reinterpret_cast<uint32_t*>(smem + xa_region_bytes(rc));
   s.acc = s.wt + twid_stride(rc.M);
   s.buf = s.acc + 2 * rc.N;
   return s;
@@ -416,6 +423,9 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     fwd_first_step<T, A, PR>(S.buf, L, rc, S.wt);
 #endif
     fwd_mid_stages<T, A, PR>(S.buf, L, rc, S.wt);
+    // the staged mask is dead after the last rep's gathers: tell the peers they may push
+    // their CRT residues into it (the matching wait precedes our own pushes)
+    if (r == a.nreps - 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     // ---- C: last stage (span 1) in registers, MAC against the key spectra ----
     if (owner) {
       const uint32_t* ks = a.spec[r];
@@ -488,19 +498,32 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     bsum_s[k - k0] = bsum;
   }
 
-  // ---- explicit CRT across the cluster through distributed shared memory ----
-  cluster.sync();
-  const uint32_t* ry[MAXNP];
-#pragma unroll
-  for (int i = 0; i < MAXNP; ++i)
-    ry[i] = i < rc.np ? cluster.map_shared_rank(S.buf, i) : nullptr;
+  // ---- explicit CRT across the cluster through distributed shared memory (push) ----
+  // every CTA stores its residues of each peer's slice into that peer's (dead) mask
+  // buffer; one release/acquire cluster barrier later each CTA owns all np residues of
+  // its slice locally, so no CTA reads a peer's memory and none must wait for peers to exit
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // peers' masks are dead
+  {
+    uint32_t* recv = reinterpret_cast<uint32_t*>(S.xa);
+    for (int q = 0; q < rc.np; ++q) {
+      uint32_t* dst = cluster.map_shared_rank(recv, q) + (size_t)PR * 2 * per;
+      const int q0 = q * per, q1 = min(N, q0 + per);
+      for (int k = q0 + threadIdx.x; k < q1; k += blockDim.x) {
+        dst[k - q0] = S.buf[k];
+        dst[per + k - q0] = S.buf[N + k];
+      }
+    }
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  const uint32_t* recv = reinterpret_cast<const uint32_t*>(S.xa);
   for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
     uint64_t ua = 0, ub = 0;
     double fa = 0.0, fb = 0.0;
 #pragma unroll
     for (int i = 0; i < MAXNP; ++i) {
       if (i < rc.np) {
-        const uint32_t ya = ry[i][k], yb = ry[i][N + k];
+        const uint32_t ya = recv[(size_t)i * 2 * per + (k - k0)], yb = recv[(size_t)i * 2 * per + per + (k - k0)];
         ua += (uint64_t)ya * rc.pc[i].q_mod64;
         ub += (uint64_t)yb * rc.pc[i].q_mod64;
         fa += (double)ya * rc.pc[i].inv_p;
@@ -509,10 +532,9 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
     const uint64_t Av = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
     const uint64_t Bv = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
-    xout[k] = ((a.identity ? S.xa[k] : 0ull) - Av) & QMASK;
+    xout[k] = ((a.identity ? xin[k] : 0ull) - Av) & QMASK;
     xout[N + k] = (bsum_s[k - k0] - Bv) & QMASK;
   }
-  cluster.sync();
 }
 
 #ifndef SFHR_ROWS_PER_CLUSTER
@@ -614,7 +636,7 @@ __global__ void __launch_bounds__(512) ks_spectra_kernel(const __grid_constant__
 #if !defined(SFHR_KS_T)
 size_t stage_smem_bytes(const RingConst& rc) {
   const int nb = rc.l > 2 ? rc.l : 2;
-  return (size_t)rc.N * 8 + (size_t)twid_stride(rc.M) * 4 + (size_t)(2 + nb) * rc.N * 4;
+  return xa_region_bytes(rc) + (size_t)twid_stride(rc.M) * 4 + (size_t)(2 + nb) * rc.N * 4;
 }
 
 int stage_threads(const RingConst& rc) {
