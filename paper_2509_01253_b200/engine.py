@@ -21,8 +21,10 @@ the whole session on a host thread when the session opens.
 
 from __future__ import annotations
 
+import functools
 import hashlib
 import json
+import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -148,6 +150,15 @@ class _ClientKeys:
     scheme: SchemeParams
 
 
+def _serialized(fn):
+    """Run an engine entry point under the engine lock (see ServerEngine.__init__)."""
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        with self._lock:
+            return fn(self, *args, **kwargs)
+    return wrapper
+
+
 class ServerEngine:
     """Holds the model and per-client key material; executes server rounds on a B200."""
 
@@ -182,10 +193,15 @@ class ServerEngine:
         self._passes = [[DevicePass(p, self.dev) for p in lower_round(model, r)]
                         for r in range(len(model.rounds))]
         self._perm_pool = ThreadPoolExecutor(max_workers=4)
+        # The reference serves one TCP connection per thread (transport.py:136-156), so
+        # calls on different sessions may be concurrent; they share this engine's device
+        # buffers, pinned staging and stream, so they run one at a time.
+        self._lock = threading.RLock()
         self.total_key_switches = 0
 
     # -- setup ---------------------------------------------------------------
 
+    @_serialized
     def register_client(self, ksk) -> bytes:
         needed = set(required_ksk_indices(self.scheme))
         have = set(ksk.indices())
@@ -222,6 +238,7 @@ class ServerEngine:
             return np.arange(size, dtype=np.int64)
         return nat.derive_permutation(self.master_seed, session_id, round_no, size)
 
+    @_serialized
     def open_session(self, session_id: bytes, key_id: bytes) -> ModelMetadata:
         if key_id not in self.clients:
             raise ProtocolError(ERR_BAD_SESSION, "unknown key id")
@@ -317,6 +334,7 @@ class ServerEngine:
                           bytes_up=round_req_size(self.scheme, n_chunks),
                           bytes_down=round_resp_size(self.scheme, n_packs))
 
+    @_serialized
     def server_round(self, session_id: bytes, round_no: int, bundles: list):
         """Reference ServerEngine.server_round (protocol.py:219-280): bundles in, packed cts out."""
         state = self._check_round(session_id, round_no, len(bundles))
@@ -331,6 +349,7 @@ class ServerEngine:
                 pk[1] = (pk[1] + extra.astype(np.int64).astype(np.uint64)) & np.uint64((1 << 53) - 1)
         return packed, self._stats(nks, times, len(bundles), len(packed))
 
+    @_serialized
     def server_round_wire(self, session_id: bytes, round_no: int, payload) -> tuple:
         """ROUND_REQ payload bytes -> (ROUND_RESP payload bytes, RoundStats).
 

@@ -101,3 +101,44 @@ def test_ntt_empty_batch_and_bad_shapes():
         pl.forward(torch.zeros((1, 3, 1 << 12), dtype=torch.int64, device="cuda"))
     with pytest.raises(ValueError):
         pl.forward(torch.zeros((1, 2, 1 << 12), dtype=torch.int32, device="cuda"))
+
+
+def test_concurrent_sessions_match_sequential():
+    """Three client threads on one engine (the reference's one-thread-per-connection
+    server, transport.py:136-156) get exactly the packs of a sequential run."""
+    import threading
+    from paper_2509_01253_b200.engine import ServerEngine
+    from paper_2509_01253_b200.keyswitch import KeySwitchKeySet
+    from paper_2509_01253_b200.params import GadgetParams, RingParams, SchemeParams
+    from paper_2509_01253_b200.workloads import toy_model
+    from oracle import lowering as olo
+    b, gamma = 12, 1
+    sch = osc.preset(b, gamma)
+    R = RingParams(sch.ring.t, sch.ring.alpha, sch.ring.p_bits)
+    g = GadgetParams(sch.gadget.D, sch.gadget.l)
+    mys = SchemeParams(R, sch.delta, g, gamma, sch.beta)
+    model = toy_model(b, 5)
+    clients = [opr.OracleClient(sch, seed=40 + i) for i in range(3)]
+    xs = [np.random.default_rng(50 + i).integers(0, 4, model.input_shape) for i in range(3)]
+
+    def run(server, i, out):
+        kid = server.register_client(KeySwitchKeySet(clients[i].make_ksk().keys, g, 0.0, R))
+        sid = bytes([i + 1]) * 16
+        server.open_session(sid, kid)
+        rounds = olo.build_rounds(model.layers)
+        bundles = clients[i].prepare_round(np.asarray(xs[i]).reshape(-1), rounds[0].input_len)
+        packs, _ = server.server_round(sid, 1, bundles)
+        out[i] = np.stack(packs)
+
+    seq, par = {}, {}
+    s1 = ServerEngine(model, mys, master_seed=bytes(range(32)))
+    for i in range(3):
+        run(s1, i, seq)
+    s2 = ServerEngine(model, mys, master_seed=bytes(range(32)))
+    th = [threading.Thread(target=run, args=(s2, i, par)) for i in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for i in range(3):
+        assert np.array_equal(seq[i], par[i]), i
