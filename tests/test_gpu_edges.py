@@ -118,16 +118,19 @@ def test_concurrent_sessions_match_sequential():
     g = GadgetParams(sch.gadget.D, sch.gadget.l)
     mys = SchemeParams(R, sch.delta, g, gamma, sch.beta)
     model = toy_model(b, 5)
-    clients = [opr.OracleClient(sch, seed=40 + i) for i in range(3)]
-    xs = [np.random.default_rng(50 + i).integers(0, 4, model.input_shape) for i in range(3)]
+    rounds = olo.build_rounds(model.layers)
+    ksks, bundles = [], []
+    for i in range(3):  # the client RNG draws happen once; both servers see the same uploads
+        cl = opr.OracleClient(sch, seed=40 + i)
+        ksks.append(cl.make_ksk())
+        x = np.random.default_rng(50 + i).integers(0, 4, model.input_shape)
+        bundles.append(cl.prepare_round(np.asarray(x).reshape(-1), rounds[0].input_len))
 
     def run(server, i, out):
-        kid = server.register_client(KeySwitchKeySet(clients[i].make_ksk().keys, g, 0.0, R))
+        kid = server.register_client(KeySwitchKeySet(ksks[i].keys, g, 0.0, R))
         sid = bytes([i + 1]) * 16
         server.open_session(sid, kid)
-        rounds = olo.build_rounds(model.layers)
-        bundles = clients[i].prepare_round(np.asarray(xs[i]).reshape(-1), rounds[0].input_len)
-        packs, _ = server.server_round(sid, 1, bundles)
+        packs, _ = server.server_round(sid, 1, bundles[i])
         out[i] = np.stack(packs)
 
     seq, par = {}, {}
