@@ -18,6 +18,8 @@ Sections (one JSON line per measurement, then a summary line):
 * mac   — ct x pt multiply-accumulate over 64 plaintexts: int_matmul_mod_q
           with a 64 x 64 integer matrix over 64 ciphertext rows (tensor cores).
 * extract — partial_extract of a full chunk (N rows).
+* client  — the client's s * a key product for one ResNet-20 inference's packs on the GPU
+          (client_ops.KeyMul) vs the reference's float64-limb algorithm on the host.
 
 Timing: CUDA events on the launching stream, warm-up first, L2 flushed
 (256 MiB write) before every timed launch; inputs are seeded uniform residues
@@ -165,9 +167,37 @@ def bench_ks(tm, quick):
     return out
 
 
+def bench_client(tm):
+    """Client-side key product s * a for the packs of one ResNet-20 inference (645 polys, b=12):
+    the GPU operator (tcgen05 linear map, host copies included) vs the reference algorithm
+    (three float64 limb GEMMs, numpy/BLAS on the host)."""
+    import time
+    from oracle import keyswitch as oks
+    from oracle import scheme as osc
+    from paper_2509_01253_b200.client_ops import KeyMul
+    from paper_2509_01253_b200.params import RingParams
+    R = osc.preset(12, 0).ring
+    sk = oks.keygen(R, "binary", seed=1)
+    km = KeyMul(sk.s, RingParams(R.t, R.alpha, R.p_bits))
+    v = np.random.default_rng(0).integers(0, 1 << 53, (645, R.N), dtype=np.uint64)
+    km.times(v)
+    t0 = time.perf_counter()
+    got = km.times(v)
+    t_gpu = time.perf_counter() - t0
+    oks.key_times(sk, v[:1])
+    t0 = time.perf_counter()
+    want = oks.key_times(sk, v)
+    t_cpu = time.perf_counter() - t0
+    assert np.array_equal(got, want)
+    out = {"section": "client", "op": "s*a mod Phi_M, 645 polys, b=12", "gpu_s": round(t_gpu, 4),
+           "cpu_reference_algorithm_s": round(t_cpu, 4)}
+    print(json.dumps(out), flush=True)
+    return [out]
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--sections", default="ntt,ks")
+    ap.add_argument("--sections", default="ntt,ks,client")
     ap.add_argument("--quick", action="store_true")
     a = ap.parse_args()
     import torch
@@ -178,6 +208,8 @@ def main():
         res += bench_ntt(tm, a.quick)
     if "ks" in a.sections:
         res += bench_ks(tm, a.quick)
+    if "client" in a.sections:
+        res += bench_client(tm)
     ntt = [r for r in res if r["section"] == "ntt" and r["batch"] >= 64]
     summ = {"summary": "primitives", "ntt_best_GB/s": max((r["GB/s"] for r in ntt), default=None),
             "ntt_best_frac": max((r["roofline"]["frac"] for r in ntt), default=None),
