@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+import threading
 
 import numpy as np
 import torch
@@ -60,6 +61,7 @@ class _Pinned:
 
 _in_stage = _Pinned()
 _out_stage = _Pinned()
+_stage_lock = threading.Lock()  # the pinned staging buffers are shared by all callers
 
 
 def parse_round_req(payload, n: int):
@@ -108,9 +110,12 @@ def decode_round_req_device(payload, n: int, device) -> tuple[torch.Tensor, list
     if k == 0:
         return torch.zeros((0, 0, 2, n), dtype=torch.int64, device=dev), exps, gammas
     size = ((len(payload) + 3) & ~3) + 4  # whole words plus the kernel's 4-byte read slack
-    stage = _in_stage.get(size)
-    stage[:len(payload)].numpy()[:] = np.frombuffer(payload, dtype=np.uint8)
-    raw = stage.to(dev, non_blocking=True)
+    with _stage_lock:
+        stage = _in_stage.get(size)
+        stage[:len(payload)].numpy()[:] = np.frombuffer(payload, dtype=np.uint8)
+        raw = stage.to(dev, non_blocking=True)
+        # the pinned buffer is reused by the next caller: the copy must have landed
+        torch.cuda.current_stream(dev).synchronize()
     offs_dev = torch.tensor(offs, dtype=torch.int64).to(dev, non_blocking=True)
     out = torch.empty((k, len(exps), 2, n), dtype=torch.int64, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -125,8 +130,13 @@ def decode_round_req_device(payload, n: int, device) -> tuple[torch.Tensor, list
 def encode_round_resp_device(packs: torch.Tensor, m: int, gamma: int) -> bytes:
     """(count, 2, N) int64 device packs -> ROUND_RESP payload bytes (wire.py:240-242)."""
     count = int(packs.shape[0])
-    n = int(packs.shape[2]) if count else 0
     size = 4 + block_size(m, count)
+    with _stage_lock:
+        return _encode_locked(packs, m, gamma, count, size)
+
+
+def _encode_locked(packs: torch.Tensor, m: int, gamma: int, count: int, size: int) -> bytes:
+    n = int(packs.shape[2]) if count else 0
     host = _out_stage.get(size)
     hv = host.numpy()
     hv[:12] = np.frombuffer(struct.pack("<III", count, m, count), dtype=np.uint8)
