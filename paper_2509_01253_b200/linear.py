@@ -52,13 +52,31 @@ def _pack_umma_k_major(wt: np.ndarray, n_pad: int, k_pad: int) -> np.ndarray:
     return np.ascontiguousarray(b.reshape(n_pad // 8, 8, k_pad // 16, 16).transpose(2, 0, 1, 3)).reshape(-1)
 
 
-def split_mma_tiles(ps: LinearPass):
-    """Merge runs of shared-column groups into tcgen05 tile groups.
+# Cost model for merging tile groups (per 16-lane M-tile, in SM clocks): the cp.async gather of one
+# 128-byte tap ~ MMA_GATHER_CLK (measured: ~20 B/clk/SM on the producer path), the tensor work of one
+# tap ~ N_pad / 64 (8192 int8 MAC/clk/SM).  Merging pixels whose column windows overlap (3x3 convs)
+# trades extra (zero-weight) MACs for fewer gathered taps per output row.
+MMA_GATHER_CLK = float(os.environ.get("SFHR_MMA_GATHER_CLK", "6.5"))
+# rows of a tile group that merges different column lists (A/B on B200, ResNet-20 linear ms per
+# inference: 9.44 unmerged, 7.64 at 64 rows / 2x2 pixel blocks, 8.5-10.9 at 96-256 rows)
+MMA_RUN_ROWS = int(os.environ.get("SFHR_MMA_RUN_ROWS", "64"))
+MMA_B_RESIDENT = 96 * 1024  # csrc/linear_mma.cu B_RESIDENT_MAX
 
-    Returns (rest_group_indices, MmaTiles | None).  A run qualifies when its
-    groups share one column list (conv pixels: every output-channel chunk;
-    fc / dense: all row chunks), |w| <= 127 (s8 B operand) and the weights fit
-    in shared memory; everything else stays on the CUDA-core kernel.
+
+def _run_cost(k_pad: int, n_pad: int, rows: int) -> float:
+    return max(MMA_GATHER_CLK * k_pad, k_pad * n_pad / 64.0) / rows
+
+
+def split_mma_tiles(ps: LinearPass):
+    """Merge runs of groups into tcgen05 tile groups.
+
+    Returns (rest_group_indices, MmaTiles | None).  A run of consecutive groups
+    becomes one tile group over the union of their column lists (conv: the
+    output-channel chunks of a pixel, then neighbouring pixels of the lowering's
+    pixel blocks, whose 3x3 windows overlap; fc / dense: all row chunks) while
+    the cost model above improves, N <= 256 and the s8 weights stay resident in
+    shared memory.  Runs with |w| > 127 and per-row column lists (pooling,
+    identity) stay on the CUDA-core kernel.
     """
     g = ps.groups
     G = len(g)
@@ -69,6 +87,12 @@ def split_mma_tiles(ps: LinearPass):
     cache = {}
     ncols = nrows = nw = 0
     max_np = max_kp = 0
+
+    def gcols(q):
+        c0, nc = int(g[q][0]), int(g[q][1])
+        c = ps.cols[c0:c0 + nc].astype(np.int64)
+        return c[c >= 0]
+
     i = 0
     while i < G:
         c0, nc, w0, r0, nr, per = (int(x) for x in g[i])
@@ -76,16 +100,28 @@ def split_mma_tiles(ps: LinearPass):
             rest.append(i)
             i += 1
             continue
-        cols = ps.cols[c0:c0 + nc]
         run, tot, j = [i], nr, i + 1
+        union = np.unique(gcols(i))
+        best = _run_cost((len(union) + 31) // 32 * 32, (tot + 15) // 16 * 16, tot)
+        all_same = True
         while j < G:
             cj, ncj, _, _, nrj, perj = (int(x) for x in g[j])
-            if perj or ncj != nc or tot + nrj > MMA_MAX_ROWS:
+            if perj or ncj == 0 or tot + nrj > MMA_MAX_ROWS:
                 break
-            if cj != c0 and not np.array_equal(ps.cols[cj:cj + ncj], cols):
+            same = ncj == nc and (cj == c0 or np.array_equal(ps.cols[cj:cj + ncj], ps.cols[c0:c0 + nc]))
+            all_same = all_same and same
+            if not all_same and tot + nrj > MMA_RUN_ROWS:
+                break
+            u2 = union if same else np.union1d(union, gcols(j))
+            k2, n2 = (len(u2) + 31) // 32 * 32, (tot + nrj + 15) // 16 * 16
+            if k2 > MMA_MAX_KPAD or (n2 * k2 > MMA_B_RESIDENT and not same):
+                break
+            c2 = _run_cost(k2, n2, tot + nrj)
+            if not same and c2 > 0.98 * best:
                 break
             run.append(j)
             tot += nrj
+            union, best = u2, min(best, c2)
             j += 1
         rows_run = np.concatenate([ps.rows[int(g[q][3]):int(g[q][3]) + int(g[q][4])] for q in run])
         # residual extras (CSR into the round input) become extra taps
@@ -98,39 +134,42 @@ def split_mma_tiles(ps: LinearPass):
                 ex_vals = np.zeros((tot, len(ex_cols)), np.int64)
                 for ri, (a, b) in enumerate(zip(lo, hi)):
                     np.add.at(ex_vals[ri], np.searchsorted(ex_cols, ps.ex_col[a:b]), ps.ex_w[a:b])
-        nc4 = (nc + 3) // 4 * 4 if len(ex_cols) else nc  # TMA gathers 4 taps of one input at a time
-        kk = nc4 + len(ex_cols)
+        nu = len(union)
+        nu4 = (nu + 3) // 4 * 4 if len(ex_cols) else nu  # TMA gathers 4 taps of one input at a time
+        kk = nu4 + len(ex_cols)
         k_pad = (kk + 31) // 32 * 32
         n_pad = (tot + 15) // 16 * 16
-        key = tuple(int(g[q][2]) for q in run) + tuple(int(g[q][4]) for q in run)
+        wt = np.zeros((tot, kk), np.int64)
+        ro = 0
+        for q in run:
+            cq, ncq, wq, _, nrq, _ = (int(x) for x in g[q])
+            cl = ps.cols[cq:cq + ncq].astype(np.int64)
+            blk = wv[wq:wq + ncq * ROWS_PER_GROUP].reshape(ncq, ROWS_PER_GROUP)[:, :nrq].astype(np.int64)
+            ok = cl >= 0
+            pos = np.searchsorted(union, cl[ok])
+            sub = np.zeros((nrq, nu), np.int64)
+            np.add.at(sub.T, pos, blk[ok])
+            wt[ro:ro + nrq, :nu] = sub
+            ro += nrq
         if ex_vals is not None:
-            key = None
-        if key is not None and key in cache:
-            woff = cache[key]
-        else:
-            wt = np.concatenate([wv[int(g[q][2]):int(g[q][2]) + nc * ROWS_PER_GROUP]
-                                 .reshape(nc, ROWS_PER_GROUP)[:, :int(g[q][4])].T for q in run])
-            if ex_vals is not None:
-                wt = np.concatenate([wt, np.zeros((tot, nc4 - nc), np.int64), ex_vals], axis=1)
-            if np.abs(wt).max(initial=0) > 127 or k_pad > MMA_MAX_KPAD or len(ex_cols) > 256:
-                rest.extend(run)
-                i = j
-                continue
-            if key is None:  # identical extras structure repeats per pixel: cache on the weights
-                key = ("w", wt.tobytes(), n_pad, k_pad)
-                woff = cache.get(key)
-            else:
-                woff = None
-            if woff is None:
-                woff = nw
-                packed = _pack_umma_k_major(wt.astype(np.int8), n_pad, k_pad)
-                tw.append(packed)
-                nw += packed.size
-                cache[key] = woff
+            wt[:, nu4:] = ex_vals
+        if np.abs(wt).max(initial=0) > 127 or k_pad > MMA_MAX_KPAD or len(ex_cols) > 256:
+            rest.extend(run)
+            i = j
+            continue
+        w8 = wt.astype(np.int8)
+        key = (n_pad, k_pad, w8.tobytes())  # interior pixel blocks share one weight operand
+        woff = cache.get(key)
+        if woff is None:
+            woff = nw
+            packed = _pack_umma_k_major(w8, n_pad, k_pad)
+            tw.append(packed)
+            nw += packed.size
+            cache[key] = woff
         tiles.append((ncols, k_pad, woff, nrows, tot, n_pad, 0, 0))
         tc = np.full(k_pad, -1, np.int64)
-        tc[:nc] = cols
-        tc[nc4:kk] = -(ex_cols + 2)
+        tc[:nu] = union
+        tc[nu4:kk] = -(ex_cols + 2)
         tcols.append(tc)
         ncols += k_pad
         trows.append(rows_run)

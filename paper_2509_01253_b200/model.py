@@ -27,6 +27,7 @@ reference's single composed matrix.
 from __future__ import annotations
 
 import json
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Optional
@@ -35,6 +36,7 @@ import numpy as np
 
 LAYER_KINDS = ("conv2d", "fully_connected", "avg_pool", "residual_add", "flatten")
 ROWS_PER_GROUP = 16
+CONV_BLOCK = int(os.environ.get("SFHR_CONV_BLOCK", "2"))  # conv output pixels lowered in 2x2 blocks
 
 
 class ModelError(Exception):
@@ -345,15 +347,18 @@ def _conv_pass(L: LayerSpec, in_len: int) -> LinearPass:
     offs = [gb.block(wmat[c0:c1]) for c0, c1 in chunks]
     ky, kx, cc = np.meshgrid(np.arange(kh), np.arange(kw), np.arange(ci), indexing="ij")
     ky, kx, cc = ky.reshape(-1), kx.reshape(-1), cc.reshape(-1)
-    for oy in range(oh):
-        iy = oy * s + ky - p
-        for ox in range(ow):
-            ix = ox * s + kx - p
-            ok = (iy >= 0) & (iy < h) & (ix >= 0) & (ix < w)
-            cols = np.where(ok, (iy * w + ix) * ci + cc, -1)
-            base = (oy * ow + ox) * co
-            for (c0, c1), off in zip(chunks, offs):
-                gb.add(cols, off, np.arange(base + c0, base + c1), cols.size, 0)
+    # output pixels in CONV_BLOCK x CONV_BLOCK blocks (raster inside a block): consecutive groups
+    # then have overlapping input windows, which the tensor-core tiler merges (linear.split_mma_tiles)
+    blk = CONV_BLOCK
+    order = [(oy, ox) for by in range(0, oh, blk) for bx in range(0, ow, blk)
+             for oy in range(by, min(oh, by + blk)) for ox in range(bx, min(ow, bx + blk))]
+    for oy, ox in order:
+        iy, ix = oy * s + ky - p, ox * s + kx - p
+        ok = (iy >= 0) & (iy < h) & (ix >= 0) & (ix < w)
+        cols = np.where(ok, (iy * w + ix) * ci + cc, -1)
+        base = (oy * ow + ox) * co
+        for (c0, c1), off in zip(chunks, offs):
+            gb.add(cols, off, np.arange(base + c0, base + c1), cols.size, 0)
     bias = None
     if L.bias is not None:
         bias = np.tile(np.asarray(L.bias, np.int64), oh * ow)

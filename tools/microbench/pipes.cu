@@ -45,6 +45,58 @@ __global__ void k_ffma(float* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_frnd(double* out, int iters) {
+  double a = threadIdx.x * 1e-3 + 0.3, c[8];
+  for (int i = 0; i < 8; ++i) c[i] = a + i * 0.37;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = rint(c[i]) + 0.3;  // FRND.F64 + DADD
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_dadd(double* out, int iters) {
+  double a = threadIdx.x * 1e-3 + 0.3, c[8];
+  for (int i = 0; i < 8; ++i) c[i] = a + i * 0.37;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c[i] = __dadd_rn(c[i], a);
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// exact FP64 modular multiply, rint vs magic-constant rounding (ops counted as 1 mulmod)
+__global__ void k_mm_rint(double* out, int iters) {
+  const double p = 1125899906826241.0, w = 987654321098765.0, wp = w / p;
+  double c[8];
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 1000.0 + i;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double h = __dmul_rn(c[i], w), l = __fma_rn(c[i], w, -h);
+      const double q = rint(__dmul_rn(c[i], wp));
+      c[i] = __dadd_rn(__fma_rn(-q, p, h), l);
+    }
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_mm_magic(double* out, int iters) {
+  const double p = 1125899906826241.0, w = 987654321098765.0, wp = w / p, mg = 6755399441055744.0;
+  double c[8];
+  for (int i = 0; i < 8; ++i) c[i] = threadIdx.x * 1000.0 + i;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double h = __dmul_rn(c[i], w), l = __fma_rn(c[i], w, -h);
+      const double q = __dadd_rn(__fma_rn(c[i], wp, mg), -mg);
+      c[i] = __dadd_rn(__fma_rn(-q, p, h), l);
+    }
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += c[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F, typename T>
 void run(const char* name, F kern, T* buf, int ops_per_iter_thread) {
   int dev = 0, sms = 0, clk = 0;
@@ -73,5 +125,9 @@ int main() {
   run("ffma", k_ffma, (float*)buf, 8);
   run("imad.wide", k_imadw, (uint64_t*)buf, 8);
   run("mulhi64", k_mulhi64, (uint64_t*)buf, 8);
+  run("frnd+dadd", k_frnd, (double*)buf, 8);
+  run("dadd", k_dadd, (double*)buf, 8);
+  run("mm_rint", k_mm_rint, (double*)buf, 8);
+  run("mm_magic", k_mm_magic, (double*)buf, 8);
   return 0;
 }
