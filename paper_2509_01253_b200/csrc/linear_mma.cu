@@ -135,7 +135,7 @@ __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_
 
 // byte offsets of the dynamic shared-memory carve-up (host and device agree)
 struct MmaSmem {
-  int ring, stage, bstage, b, ep, colp, odst, ocan, bars, tslot, total;
+  int ring, stage, bstage, b, ep, colp, odst, obias, bars, tslot, total;
   bool stream;  // B streamed per stage (stage = A 8 KB + B chunk Np x 64 B) instead of resident
   __host__ __device__ static MmaSmem make(int Np, int Kp) {
     MmaSmem s;
@@ -147,8 +147,8 @@ struct MmaSmem {
     s.ep = s.b + (s.stream ? 0 : ((Np * Kp + 127) & ~127));
     s.colp = s.ep + EPI_WARPS * EP_COLS * 32 * 4;
     s.odst = s.colp + Kp * 8;
-    s.ocan = s.odst + Np * 8;
-    s.bars = (s.ocan + Np * 4 + 7) & ~7;
+    s.obias = s.odst + Np * 8;
+    s.bars = s.obias + Np * 8;
     s.tslot = s.bars + (2 * NSTAGE + 4) * 8;
     s.total = s.tslot + 16 + 1024;  // + alignment slack for the 1024-B swizzle atoms
     return s;
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   const int SB = L.stage;  // bytes per pipeline stage
   const unsigned char** colp = reinterpret_cast<const unsigned char**>(sm + L.colp);
   int64_t* odst = reinterpret_cast<int64_t*>(sm + L.odst);
-  int32_t* ocan = reinterpret_cast<int32_t*>(sm + L.ocan);
+  int64_t* obias = reinterpret_cast<int64_t*>(sm + L.obias);
   // barriers: full[NSTAGE] (128 producer arrivals), empty[NSTAGE] (MMA commit),
   // acc_full[2] (MMA commit), acc_empty[2] (4 epilogue warps)
   const uint32_t bars = su32(sm + L.bars);
@@ -215,10 +215,10 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
   for (int o = tid; o < Np; o += MMA_THREADS) {
     if (o < nr) {
       const int r = a.trows[r0 + o];
-      ocan[o] = r;
-      odst[o] = a.out_map ? a.out_map[r] : (int64_t)r;
+      obias[o] = a.bias ? a.bias[r] : 0;
+      odst[o] = (a.out_map ? a.out_map[r] : (int64_t)r) * lanes;  // element offset of the output row
     } else {
-      ocan[o] = -1;
+      obias[o] = 0;
       odst[o] = -1;
     }
   }
@@ -357,6 +357,9 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
       mbar_wait(accf0 + 8 * buf, (uint32_t)((mtl >> 1) & 1));
       tc_fence_after();
       const int64_t lane0 = (int64_t)(mt0 + mtl) * 16 + warp * 4;  // this warp's 4 u64 lanes
+      const int64_t ln = lane0 + (lane & 3);                         // this thread's lane (both h)
+      const bool lane_ok = ln < lanes;
+      const uint64_t unitv = (a.bias && lane_ok && ln >= a.body_off) ? a.unit[ln - a.body_off] : 0ull;
       for (int cc = 0; cc < Np; cc += EP_COLS) {
         uint32_t r[16];
         tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * Np + cc), r);
@@ -368,14 +371,13 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
           const int idx = lane + 32 * h;
           const int cl = idx >> 2, u = idx & 3;
           const int o = cc + cl;
-          const int64_t ln = lane0 + u;
-          if (o < nr && ln < lanes) {
+          if (o < nr && lane_ok) {
             const int4* p = reinterpret_cast<const int4*>(ep + cl * 32 + u * 8);
             const int4 x0 = p[0], x1 = p[1];
             uint64_t v = sx(x0.x) + (sx(x0.y) << 8) + (sx(x0.z) << 16) + (sx(x0.w) << 24) +
                          (sx(x1.x) << 32) + (sx(x1.y) << 40) + (sx(x1.z) << 48) + (sx(x1.w) << 56);
-            if (a.bias && ln >= a.body_off) v += (uint64_t)a.bias[ocan[o]] * a.unit[ln - a.body_off];
-            a.out[odst[o] * lanes + ln] = v & QMASK;
+            v += (uint64_t)obias[o] * unitv;
+            a.out[odst[o] + ln] = v & QMASK;
           }
         }
         __syncwarp();
