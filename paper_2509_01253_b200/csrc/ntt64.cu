@@ -89,6 +89,26 @@ __device__ __forceinline__ void gs_bfly(double& X, double& Y, double w, double w
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 4); }  // one pad word per 16 (bank spread)
 
+// The 2^st twiddles of one sub-butterfly stage are consecutive and 2^st-aligned in the table:
+// 16-byte vector loads, and only w is loaded.  Its Shoup companion w / p is formed in registers
+// as w * (1/p) (two roundings instead of one: x * wp stays within 1.5 of x w / p for the
+// |x| < 2p inputs the passes feed mulmod_d, so the quotient is off by at most 2 and every
+// intermediate stays far below 2^52; the final residues are exact either way).
+// (K is a constant after the callers' loops unroll)
+__device__ __forceinline__ void load_twiddles(int K, double* tw, const double* src) {
+  if (K == 1) {
+    tw[0] = __ldg(src);
+  } else {
+#pragma unroll
+    for (int t = 0; t < 8; t += 2) {
+      if (t >= K) break;
+      const double2 q = __ldg(reinterpret_cast<const double2*>(src + t));
+      tw[t] = q.x;
+      tw[t + 1] = q.y;
+    }
+  }
+}
+
 // Twiddles of one radix-2^r sub-butterfly: for the pass's stage st (global stage
 // s0 + st, distance d = D >> st) the 2^st groups it touches are
 // g = B0 / (2d) + t, t < 2^st (B0 = global start of its 2D block), i.e. the
@@ -113,7 +133,7 @@ __device__ __forceinline__ void fwd_local(double* sm, int64_t c0, int s0, const 
     const int per = EPT >> r;                   // independent sub-butterflies per thread
     double v[EPT];
     int base[EPT >> 1];
-    double tw[EPT >> 1][15], twp[EPT >> 1][15];
+    double tw[EPT >> 1][15];
 #pragma unroll
     for (int h = 0; h < per; ++h) {
       const int id = threadIdx.x * per + h;
@@ -123,11 +143,7 @@ __device__ __forceinline__ void fwd_local(double* sm, int64_t c0, int s0, const 
 #pragma unroll
       for (int st = 0; st < r; ++st) {
         const int64_t k0 = ((int64_t)1 << (s0 + done + st)) + (B0 >> (logD + 1 - st));
-#pragma unroll
-        for (int t = 0; t < (1 << st); ++t) {
-          tw[h][(1 << st) - 1 + t] = __ldg(w + k0 + t);
-          twp[h][(1 << st) - 1 + t] = __ldg(wp + k0 + t);
-        }
+        load_twiddles(1 << st, tw[h] + (1 << st) - 1, w + k0);
       }
 #pragma unroll
       for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = red_d(sm[pad(base[h] + lo * inner)], p, pinv);
@@ -137,11 +153,14 @@ __device__ __forceinline__ void fwd_local(double* sm, int64_t c0, int s0, const 
       const int half = (1 << r) >> (st + 1);    // distance in lo units
 #pragma unroll
       for (int h = 0; h < per; ++h) {
+        double twp[8];  // w / p of this stage's twiddles (see load_twiddles)
+#pragma unroll
+        for (int t = 0; t < (1 << st); ++t) twp[t] = __dmul_rn(tw[h][(1 << st) - 1 + t], pinv);
 #pragma unroll
         for (int lo = 0; lo < (1 << r); ++lo) {
           if (lo & half) continue;
           const int t = (1 << st) - 1 + (lo >> (r - st));
-          ct_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], twp[h][t], p);
+          ct_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], twp[lo >> (r - st)], p);
         }
       }
       if (st == 1 && r > 2) {
@@ -173,7 +192,7 @@ __device__ __forceinline__ void inv_local(double* sm, int64_t c0, int s0, const 
     const int per = EPT >> r;
     double v[EPT];
     int base[EPT >> 1];
-    double tw[EPT >> 1][15], twp[EPT >> 1][15];
+    double tw[EPT >> 1][15];
 #pragma unroll
     for (int h = 0; h < per; ++h) {
       const int id = threadIdx.x * per + h;
@@ -185,11 +204,7 @@ __device__ __forceinline__ void inv_local(double* sm, int64_t c0, int s0, const 
       for (int u = 0; u < r; ++u) {
         const int s = s0 + LOGC - 1 - (done + r - 1 - u);
         const int64_t k0 = ((int64_t)1 << s) + (B0 >> (logD + 1 - u));
-#pragma unroll
-        for (int t = 0; t < (1 << u); ++t) {
-          tw[h][(1 << u) - 1 + t] = __ldg(w + k0 + t);
-          twp[h][(1 << u) - 1 + t] = __ldg(wp + k0 + t);
-        }
+        load_twiddles(1 << u, tw[h] + (1 << u) - 1, w + k0);
       }
 #pragma unroll
       for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = red_d(sm[pad(base[h] + lo * inner)], p, pinv);
@@ -200,11 +215,14 @@ __device__ __forceinline__ void inv_local(double* sm, int64_t c0, int s0, const 
       const int u = r - 1 - st;
 #pragma unroll
       for (int h = 0; h < per; ++h) {
+        double twp[8];
+#pragma unroll
+        for (int t = 0; t < (1 << u); ++t) twp[t] = __dmul_rn(tw[h][(1 << u) - 1 + t], pinv);
 #pragma unroll
         for (int lo = 0; lo < (1 << r); ++lo) {
           if (lo & half) continue;
           const int t = (1 << u) - 1 + (lo >> (st + 1));
-          gs_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], twp[h][t], p);
+          gs_bfly(v[h * (1 << r) + lo], v[h * (1 << r) + lo + half], tw[h][t], twp[lo >> (st + 1)], p);
         }
       }
       if (st == 1 && r > 2) {
