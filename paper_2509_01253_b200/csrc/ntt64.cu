@@ -252,7 +252,11 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd
   const double* wp = t.wp + (size_t)limb * ((size_t)1 << LOGN);
   uint64_t* x = data + poly * ((int64_t)1 << LOGN);
   if (C == 1) {
-    for (int i = threadIdx.x; i < CH; i += NT) sm[pad(i)] = (double)x[i];
+    uint64_t in[EPT];  // all loads in flight before the first shared store
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) in[e] = x[threadIdx.x + e * NT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) sm[pad(threadIdx.x + e * NT)] = (double)in[e];
     __syncthreads();
   } else {
     // cross-chunk stages 0 .. LOGCL-1: this CTA owns chunk offsets [c*CH/C, (c+1)*CH/C)
@@ -309,9 +313,15 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_inv
   const double ninv = __ldg(w), ninvp = __ldg(wp);  // wi[0] = N^-1
   uint64_t* x = data + poly * ((int64_t)1 << LOGN);
   const uint64_t* xi = x + (int64_t)c * CH;
-  for (int i = threadIdx.x; i < CH; i += NT) {
-    const uint64_t v = xi[i];
-    sm[pad(i)] = (double)(v >= pu ? v - pu : v);  // tolerate inputs in [0, 2p)
+  {
+    uint64_t in[EPT];  // all loads in flight before the first shared store
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) in[e] = xi[threadIdx.x + e * NT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint64_t v = in[e];
+      sm[pad(threadIdx.x + e * NT)] = (double)(v >= pu ? v - pu : v);  // tolerate inputs in [0, 2p)
+    }
   }
   __syncthreads();
   inv_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, wp, p, pinv);
