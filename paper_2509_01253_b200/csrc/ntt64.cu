@@ -145,8 +145,14 @@ __device__ __forceinline__ void fwd_local(double* sm, int64_t c0, int s0, const 
         const int64_t k0 = ((int64_t)1 << (s0 + done + st)) + (B0 >> (logD + 1 - st));
         load_twiddles(1 << st, tw[h] + (1 << st) - 1, w + k0);
       }
+      // passes of >= 3 stages reduce after their second stage and store values below ~2p, and the
+      // cross-chunk stages / raw input are below ~2p too, so only the short (r <= 2) passes
+      // reduce on load: two CT stages from 2p stay below ~5p < 2^53 (see load_twiddles)
 #pragma unroll
-      for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = red_d(sm[pad(base[h] + lo * inner)], p, pinv);
+      for (int lo = 0; lo < (1 << r); ++lo) {
+        const double x = sm[pad(base[h] + lo * inner)];
+        v[h * (1 << r) + lo] = r <= 2 ? red_d(x, p, pinv) : x;
+      }
     }
 #pragma unroll
     for (int st = 0; st < r; ++st) {
