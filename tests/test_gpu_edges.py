@@ -79,6 +79,26 @@ def test_extract_one_and_full_chunk(b):
         partial_extract(bundle, None, R.N + 1, Rm)
 
 
+@pytest.mark.parametrize("b,gamma", [(8, 0), (12, 0), (16, 0), (8, 1), (12, 1)])
+def test_extract_kernels_agree(b, gamma, monkeypatch):
+    """The offset-table kernel (<= 2 powers), the tiled kernel and the oracle agree bit for bit."""
+    from paper_2509_01253_b200.params import RingParams
+    from paper_2509_01253_b200.tracepack import PowerBundle, partial_extract, power_exponents
+    from paper_2509_01253_b200.keyswitch import RlweCiphertext
+    sch = osc.preset(b, gamma)
+    R = sch.ring
+    Rm = RingParams(R.t, R.alpha, R.p_bits)
+    exps = power_exponents(gamma, Rm)
+    power = u53(91 + b, (len(exps), 2, R.N))
+    bundle = PowerBundle(gamma, {d: RlweCiphertext(power[q, 0], power[q, 1]) for q, d in enumerate(exps)})
+    obundle = opk.Bundle(gamma, {d: oks.Ct(power[q, 0], power[q, 1]) for q, d in enumerate(exps)})
+    fast = partial_extract(bundle, None, R.N, Rm)
+    monkeypatch.setenv("SFHR_EXTRACT_TILED", "1")
+    tiled = partial_extract(bundle, None, R.N, Rm)
+    assert np.array_equal(fast, tiled)
+    assert np.array_equal(fast, opk.extract(obundle, R.N, R))
+
+
 def test_missing_key_index_raises():
     sch, ksk, eng = _engine(12, 1)
     N = sch.ring.N
