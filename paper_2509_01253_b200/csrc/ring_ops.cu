@@ -193,23 +193,33 @@ __global__ void __launch_bounds__(EX_THREADS) extract_tiled_kernel(const __grid_
 
 size_t extract_tiled_smem(const RingConst& rc, int npow) { return (size_t)npow * 2 * rc.M * 8; }
 
-// Offset-table variant for few powers (gamma = 0: one power): each power ciphertext is staged
-// as an EXTENDED array e[j] = ct[j mod M] (0 where j mod M >= N) of length M + N, so the four
-// reads of a (row, power) are e[o + k] with the row's four rotation offsets o < M precomputed
-// once per CTA (x0 = i d, y0 = i d - c_i n1 d, x1 = i d + N, y1 = x1 - c_i n1 d, all mod M) and
-// k (or k mod n1 for the folded pair) the thread's lane: no modular index arithmetic per
-// element, ~4x fewer instructions than extract_tiled_kernel, leaving the HBM row writes.
-constexpr int EXX_MAXPOW = 2;  // template instances NP = 1, 2
+// Offset-table variant (up to 6 powers): each power ciphertext is staged as an EXTENDED array
+// e[j] = cu * ct[j mod M] (0 where j mod M >= N) of length M + N, so the four reads of a
+// (row, power) are e[o + k] with the row's four rotation offsets o < M precomputed once per
+// CTA (x0 = i d, y0 = i d - c_i n1 d, x1 = i d + N, y1 = x1 - c_i n1 d, all mod M) and k (or
+// k mod n1 for the folded pair) the thread's lane: no modular index arithmetic per element
+// (~27 instead of ~98 instructions per output at one power).  When both components of all
+// powers do not fit in shared memory (SPLIT) the CTA stages and processes one component at a
+// time.  M^-1 (cu) is folded into the staged values: (sum +-ct) cu = sum +-(ct cu) mod 2^64.
+constexpr int EXX_MAXPOW = 6;
 #ifndef SFHR_EXX_ROWS
 #define SFHR_EXX_ROWS 16
 #endif
-constexpr int EXX_ROWS = SFHR_EXX_ROWS;  // rows per CTA: small tiles -> several waves, no tail
+constexpr int EXX_ROWS = SFHR_EXX_ROWS;  // rows per CTA (A/B on B200: 16 > 8 > 32)
+constexpr size_t EXX_SMEM_MAX = 227 * 1024;
 
-template <int NP>
-__global__ void __launch_bounds__(EX_THREADS) extract_ext_kernel(const __grid_constant__ RingConst rc,
-                                                                 const __grid_constant__ ExtractArgs a) {
-  extern __shared__ __align__(16) uint64_t se[];  // [NP][2][M + N], pre-multiplied by cu
-  __shared__ uint4 soff[EXX_ROWS][NP];            // byte offsets of the four reads
+// SPLIT kernels hold one CTA per SM: twice the threads and 4x the rows per staging of the powers
+template <bool SPLIT> struct ExxGeo {
+  static constexpr int THREADS = SPLIT ? 1024 : EX_THREADS;
+  static constexpr int ROWS = SPLIT ? 4 * EXX_ROWS : EXX_ROWS;
+};
+
+template <int NP, bool SPLIT>
+__global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(const __grid_constant__ RingConst rc,
+                                                                             const __grid_constant__ ExtractArgs a) {
+  constexpr int EXX_ROWS = ExxGeo<SPLIT>::ROWS, EX_THREADS = ExxGeo<SPLIT>::THREADS;
+  extern __shared__ __align__(16) uint64_t se[];  // [SPLIT ? 1 : 2][NP][M + N]
+  __shared__ uint4 soff[EXX_ROWS][NP];            // byte offsets of the four reads within a power
   const int N = rc.N, M = rc.M, n1 = rc.n1, L = M + N;
   const int rblocks = (N + EXX_ROWS - 1) / EXX_ROWS;
   const int j = (int)(blockIdx.x / rblocks), rb = (int)(blockIdx.x % rblocks);
@@ -217,59 +227,82 @@ __global__ void __launch_bounds__(EX_THREADS) extract_ext_kernel(const __grid_co
   const int64_t g0 = (int64_t)j * N + i0;
   if (g0 >= a.E) return;
   const int nrows = (int)min((int64_t)min(EXX_ROWS, N - i0), a.E - g0);
-  const uint64_t* src = a.power + (int64_t)j * NP * 2 * N;
-  const uint64_t cu = a.cu;  // (sum +-ct) cu = sum +-(ct cu) mod 2^64: scale once while staging
-  for (int idx = threadIdx.x; idx < NP * 2 * L; idx += EX_THREADS) {
-    const int qc = idx / L, x = idx - qc * L;
-    const int xm = x >= M ? x - M : x;
-    se[idx] = xm < N ? src[(int64_t)qc * N + xm] * cu : 0ull;
-  }
+  const uint64_t* src = a.power + (int64_t)j * NP * 2 * N;  // [NP][2][N]
+  const uint64_t cu = a.cu;
   for (int t = threadIdx.x; t < nrows * NP; t += EX_THREADS) {
     const int r = t / NP, q = t - r * NP;
     const uint32_t d = a.exps[q];
     const uint32_t id = fastmod((uint32_t)(i0 + r) * d, M, rc.magicM);
     const uint32_t sh = fastmod((uint32_t)(a.cvec[i0 + r] * n1) * d, M, rc.magicM);
     const uint32_t x1 = id + (uint32_t)N >= (uint32_t)M ? id + N - M : id + N;
-    const uint32_t qo = (uint32_t)(q * 2 * L);
-    soff[r][q] = make_uint4(8 * (qo + id), 8 * (qo + (id >= sh ? id - sh : id + M - sh)), 8 * (qo + x1),
-                            8 * (qo + (x1 >= sh ? x1 - sh : x1 + M - sh)));
+    soff[r][q] = make_uint4(8 * id, 8 * (id >= sh ? id - sh : id + M - sh), 8 * x1,
+                            8 * (x1 >= sh ? x1 - sh : x1 + M - sh));
   }
-  __syncthreads();
   const char* sb = reinterpret_cast<const char*>(se);
-  for (int lane = threadIdx.x; lane < 2 * N; lane += EX_THREADS) {
-    const int comp = lane >= N;
-    const int k = lane - comp * N;
-    const int kf = (int)fastmod((uint32_t)k, n1, rc.magicN1);
-    const char* ek = sb + 8 * (comp * L + k);
-    const char* ef = sb + 8 * (comp * L + kf);
-    uint64_t* dst = a.rows + g0 * 2 * N + lane;
+#pragma unroll 1
+  for (int part = 0; part < (SPLIT ? 2 : 1); ++part) {
+    if (SPLIT && part) __syncthreads();  // every thread is done with component 0
+    // staged layout: [comp (SPLIT: only this part's)][q][L]
+    const int ncomp = SPLIT ? 1 : 2;
+    for (int idx = threadIdx.x; idx < ncomp * NP * L; idx += EX_THREADS) {
+      const int cq = idx / L, x = idx - cq * L;
+      const int comp = SPLIT ? part : cq / NP, q = cq - (cq / NP) * NP;
+      const int xm = x >= M ? x - M : x;
+      se[idx] = xm < N ? src[((int64_t)q * 2 + comp) * N + xm] * cu : 0ull;
+    }
+    __syncthreads();
+    const int lane0 = SPLIT ? part * N : 0, lane1 = SPLIT ? lane0 + N : 2 * N;
+    for (int lane = lane0 + threadIdx.x; lane < lane1; lane += EX_THREADS) {
+      const int comp = lane >= N;
+      const int k = lane - comp * N;
+      const int kf = (int)fastmod((uint32_t)k, n1, rc.magicN1);
+      const char* ek = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + k);
+      const char* ef = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + kf);
+      uint64_t* dst = a.rows + g0 * 2 * N + lane;
 #pragma unroll 4
-    for (int r = 0; r < nrows; ++r) {
-      uint64_t acc = 0;
+      for (int r = 0; r < nrows; ++r) {
+        uint64_t acc = 0;
 #pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        const uint4 o = soff[r][q];
-        acc += (*reinterpret_cast<const uint64_t*>(ek + o.x) - *reinterpret_cast<const uint64_t*>(ek + o.y)) -
-               (*reinterpret_cast<const uint64_t*>(ef + o.z) - *reinterpret_cast<const uint64_t*>(ef + o.w));
+        for (int q = 0; q < NP; ++q) {
+          const uint4 o = soff[r][q];
+          const int qo = 8 * q * L;
+          acc += (*reinterpret_cast<const uint64_t*>(ek + qo + o.x) - *reinterpret_cast<const uint64_t*>(ek + qo + o.y)) -
+                 (*reinterpret_cast<const uint64_t*>(ef + qo + o.z) - *reinterpret_cast<const uint64_t*>(ef + qo + o.w));
+        }
+        dst[(int64_t)r * 2 * N] = acc & QMASK;
       }
-      dst[(int64_t)r * 2 * N] = acc & QMASK;
     }
   }
 }
 
-size_t extract_ext_smem(const RingConst& rc, int npow) { return (size_t)npow * 2 * (rc.M + rc.N) * 8; }
+template <int NP>
+static cudaError_t launch_ext(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
+  const size_t both = (size_t)2 * NP * (rc.M + rc.N) * 8;
+  const bool split = both > EXX_SMEM_MAX;
+  const size_t smem = split ? both / 2 : both;
+  const auto kern = split ? extract_ext_kernel<NP, true> : extract_ext_kernel<NP, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int rows = split ? ExxGeo<true>::ROWS : ExxGeo<false>::ROWS;
+  const int threads = split ? ExxGeo<true>::THREADS : ExxGeo<false>::THREADS;
+  const int rblocks = (rc.N + rows - 1) / rows;
+  kern<<<(unsigned)(a.k_chunks * rblocks), threads, smem, st>>>(rc, a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
   if (a.E == 0) return cudaSuccess;
-  // SFHR_EXTRACT_TILED=1 forces the general kernel (the tests compare both paths)
-  if (a.npow <= EXX_MAXPOW && extract_ext_smem(rc, a.npow) <= 200 * 1024 && !getenv("SFHR_EXTRACT_TILED")) {
-    const size_t xs = extract_ext_smem(rc, a.npow);
-    const auto kern = a.npow == 1 ? extract_ext_kernel<1> : extract_ext_kernel<2>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs);
-    if (e != cudaSuccess) return e;
-    const int rblocks = (rc.N + EXX_ROWS - 1) / EXX_ROWS;
-    kern<<<(unsigned)(a.k_chunks * rblocks), EX_THREADS, xs, st>>>(rc, a);
-    return cudaGetLastError();
+  // SFHR_EXTRACT_TILED=1 forces the general kernels (the tests compare both paths)
+  if (a.npow >= 1 && a.npow <= EXX_MAXPOW && (size_t)a.npow * (rc.M + rc.N) * 8 <= EXX_SMEM_MAX &&
+      !getenv("SFHR_EXTRACT_TILED")) {
+    switch (a.npow) {
+      case 1: return launch_ext<1>(rc, a, st);
+      case 2: return launch_ext<2>(rc, a, st);
+      case 3: return launch_ext<3>(rc, a, st);
+      case 4: return launch_ext<4>(rc, a, st);
+      case 5: return launch_ext<5>(rc, a, st);
+      default: return launch_ext<6>(rc, a, st);
+    }
   }
   const size_t smem = extract_tiled_smem(rc, a.npow);
   if (a.npow <= EX_MAXPOW && smem <= 200 * 1024) {
