@@ -75,8 +75,9 @@ def split_mma_tiles(ps: LinearPass):
     output-channel chunks of a pixel, then neighbouring pixels of the lowering's
     pixel blocks, whose 3x3 windows overlap; fc / dense: all row chunks) while
     the cost model above improves, N <= 256 and the s8 weights stay resident in
-    shared memory.  Runs with |w| > 127 and per-row column lists (pooling,
-    identity) stay on the CUDA-core kernel.
+    shared memory.  Runs with |w| > 127 stay on the CUDA-core kernel; per-row column
+    lists (pooling, identity) join as block-sparse tile groups over the union of their
+    rows' columns.
     """
     g = ps.groups
     G = len(g)
@@ -88,27 +89,30 @@ def split_mma_tiles(ps: LinearPass):
     ncols = nrows = nw = 0
     max_np = max_kp = 0
 
-    def gcols(q):
-        c0, nc = int(g[q][0]), int(g[q][1])
-        c = ps.cols[c0:c0 + nc].astype(np.int64)
+    def gcols(q):  # every valid input column the group reads (per-row lists concatenated)
+        c0, nc, nr, per = int(g[q][0]), int(g[q][1]), int(g[q][4]), int(g[q][5])
+        c = ps.cols[c0:c0 + (nr * nc if per else nc)].astype(np.int64)
         return c[c >= 0]
 
     i = 0
     while i < G:
         c0, nc, w0, r0, nr, per = (int(x) for x in g[i])
-        if per or nc == 0:
+        if nc == 0:
             rest.append(i)
             i += 1
             continue
+        # per-row column lists (pooling, identity) become a tile group over their union with
+        # block-sparse weights: each input row is still gathered once per output group
         run, tot, j = [i], nr, i + 1
         union = np.unique(gcols(i))
         best = _run_cost((len(union) + 31) // 32 * 32, (tot + 15) // 16 * 16, tot)
-        all_same = True
+        all_same = not per
         while j < G:
             cj, ncj, _, _, nrj, perj = (int(x) for x in g[j])
-            if perj or ncj == 0 or tot + nrj > MMA_MAX_ROWS:
+            if ncj == 0 or tot + nrj > MMA_MAX_ROWS:
                 break
-            same = ncj == nc and (cj == c0 or np.array_equal(ps.cols[cj:cj + ncj], ps.cols[c0:c0 + nc]))
+            same = not per and not perj and ncj == nc and (
+                cj == c0 or np.array_equal(ps.cols[cj:cj + ncj], ps.cols[c0:c0 + nc]))
             all_same = all_same and same
             if not all_same and tot + nrj > MMA_RUN_ROWS:
                 break
@@ -142,13 +146,17 @@ def split_mma_tiles(ps: LinearPass):
         wt = np.zeros((tot, kk), np.int64)
         ro = 0
         for q in run:
-            cq, ncq, wq, _, nrq, _ = (int(x) for x in g[q])
-            cl = ps.cols[cq:cq + ncq].astype(np.int64)
+            cq, ncq, wq, _, nrq, perq = (int(x) for x in g[q])
             blk = wv[wq:wq + ncq * ROWS_PER_GROUP].reshape(ncq, ROWS_PER_GROUP)[:, :nrq].astype(np.int64)
-            ok = cl >= 0
-            pos = np.searchsorted(union, cl[ok])
             sub = np.zeros((nrq, nu), np.int64)
-            np.add.at(sub.T, pos, blk[ok])
+            if perq:  # row i reads cols[cq + i*ncq : ...] with weights blk[:, i]
+                cl = ps.cols[cq:cq + nrq * ncq].astype(np.int64).reshape(nrq, ncq)
+                ok = cl >= 0
+                np.add.at(sub, (np.nonzero(ok)[0], np.searchsorted(union, cl[ok])), blk.T[ok])
+            else:
+                cl = ps.cols[cq:cq + ncq].astype(np.int64)
+                ok = cl >= 0
+                np.add.at(sub.T, np.searchsorted(union, cl[ok]), blk[ok])
             wt[ro:ro + nrq, :nu] = sub
             ro += nrq
         if ex_vals is not None:
