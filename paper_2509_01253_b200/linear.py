@@ -60,6 +60,7 @@ MMA_GATHER_CLK = float(os.environ.get("SFHR_MMA_GATHER_CLK", "6.5"))
 # rows of a tile group that merges different column lists (A/B on B200, ResNet-20 linear ms per
 # inference: 9.44 unmerged, 7.64 at 64 rows / 2x2 pixel blocks, 8.5-10.9 at 96-256 rows)
 MMA_RUN_ROWS = int(os.environ.get("SFHR_MMA_RUN_ROWS", "64"))
+MMA_SAME_ROWS = int(os.environ.get("SFHR_MMA_SAME_ROWS", str(MMA_MAX_ROWS)))  # runs sharing one list
 MMA_B_RESIDENT = 96 * 1024  # csrc/linear_mma.cu B_RESIDENT_MAX
 
 
@@ -109,7 +110,7 @@ def split_mma_tiles(ps: LinearPass):
         all_same = not per
         while j < G:
             cj, ncj, _, _, nrj, perj = (int(x) for x in g[j])
-            if ncj == 0 or tot + nrj > MMA_MAX_ROWS:
+            if ncj == 0 or tot + nrj > min(MMA_MAX_ROWS, MMA_SAME_ROWS):
                 break
             same = not per and not perj and ncj == nc and (
                 cj == c0 or np.array_equal(ps.cols[cj:cj + ncj], ps.cols[c0:c0 + nc]))
