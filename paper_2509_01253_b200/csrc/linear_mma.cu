@@ -37,7 +37,10 @@ constexpr int EPI_WARPS = 4;              // TMEM lanes 0-127
 constexpr int PRODUCERS = SFHR_MMA_PRODUCERS;  // cp.async gather threads
 constexpr int MMA_THREADS = EPI_WARPS * 32 + PRODUCERS + 32;
 constexpr int KC = 64;                    // taps per pipeline stage (2 MMAs)
-constexpr int NSTAGE = 4;
+#ifndef SFHR_MMA_NSTAGE
+#define SFHR_MMA_NSTAGE 4
+#endif
+constexpr int NSTAGE = SFHR_MMA_NSTAGE;  // pipeline depth (bytes in flight bound the gather rate)
 constexpr int STAGE_BYTES = KC * 128;     // 8 KB of A per stage
 constexpr int B_RESIDENT_MAX = 96 * 1024; // larger weight operands are streamed with each stage
 constexpr int EP_COLS = 16;               // accumulator columns per epilogue chunk
@@ -113,6 +116,10 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 
 __device__ __forceinline__ uint64_t sx(int v) { return (uint64_t)(int64_t)v; }
 
+// raise the stage's expected transaction bytes without arriving (the cp.async producers arrive)
+__device__ __forceinline__ void mbar_add_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -292,11 +299,13 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
         const int ntaps = min(KC, Kp - kc * KC);
         const unsigned char* const* cp = colp + kc * KC;
         const uint32_t dst = ring + stage * SB + dst_lane;
-        if (L.stream) {  // this stage's B chunk: K blocks 4kc.. of the packed [K/16][N/8][8][16] weights
+        if (L.stream && pt == 0) {  // this stage's B chunk (contiguous K blocks 4kc.. of the packed
+          // [K/16][N/8][8][16] weights): one bulk copy on the stage's barrier, tx counted before
+          // this thread's own arrival so the phase cannot complete without it
           const int kb0 = kc * (KC / 16), nkb = min(KC, Kp - kc * KC) / 16;
-          const unsigned char* bsrc = wsrc + (size_t)kb0 * (Np / 8) * 128;
-          const uint32_t bdst = ring + stage * SB + STAGE_BYTES;
-          for (int i = pt; i < nkb * (Np / 8) * 8; i += PRODUCERS) cp16(bdst + 16 * i, bsrc + 16 * i, 16);
+          const uint32_t bbytes = (uint32_t)(nkb * (Np / 8) * 128);
+          mbar_add_tx(full0 + 8 * stage, bbytes);
+          bulk_copy(ring + stage * SB + STAGE_BYTES, wsrc + (size_t)kb0 * (Np / 8) * 128, bbytes, full0 + 8 * stage);
         }
         constexpr int TSTRIDE = PRODUCERS / 8;  // taps covered by one sweep of the producers
 #pragma unroll
