@@ -193,14 +193,15 @@ __global__ void __launch_bounds__(EX_THREADS) extract_tiled_kernel(const __grid_
 
 size_t extract_tiled_smem(const RingConst& rc, int npow) { return (size_t)npow * 2 * rc.M * 8; }
 
-// Offset-table variant (up to 6 powers): each power ciphertext is staged as an EXTENDED array
-// e[j] = cu * ct[j mod M] (0 where j mod M >= N) of length M + N, so the four reads of a
-// (row, power) are e[o + k] with the row's four rotation offsets o < M precomputed once per
-// CTA (x0 = i d, y0 = i d - c_i n1 d, x1 = i d + N, y1 = x1 - c_i n1 d, all mod M) and k (or
-// k mod n1 for the folded pair) the thread's lane: no modular index arithmetic per element
-// (~27 instead of ~98 instructions per output at one power).  When both components of all
-// powers do not fit in shared memory (SPLIT) the CTA stages and processes one component at a
-// time.  M^-1 (cu) is folded into the staged values: (sum +-ct) cu = sum +-(ct cu) mod 2^64.
+// Offset-table variant (up to 6 powers).  Row i needs, per power d, (ct[x0] - ct[x0 - s]) -
+// (ct[x1] - ct[x1 - s]) at x0 = i d + k, x1 = i d + N + (k mod n1), s = c_i n1 d (mod M).  c_i
+// is constant over long runs of rows, so per distinct c of the CTA's row tile each power is
+// staged once as the DIFFERENCE array D[x] = cu (ct[x mod M] - ct[(x - s) mod M]) (ct = 0 at
+// indices >= N), extended to length M + N so that both reads are D[o + k] / D[o' + k mod n1]
+// with per-(row, power) offsets o = i d, o' = i d + N precomputed once: 2 shared loads and 2
+// adds per (output, power), no modular index arithmetic per element.  When both components of
+// all powers do not fit in shared memory (SPLIT) the CTA stages one component at a time.
+// M^-1 (cu) is folded into the staged values: (sum +-ct) cu = sum +-(ct cu) mod 2^64.
 constexpr int EXX_MAXPOW = 6;
 #ifndef SFHR_EXX_ROWS
 #define SFHR_EXX_ROWS 16
@@ -218,8 +219,10 @@ template <int NP, bool SPLIT>
 __global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(const __grid_constant__ RingConst rc,
                                                                              const __grid_constant__ ExtractArgs a) {
   constexpr int EXX_ROWS = ExxGeo<SPLIT>::ROWS, EX_THREADS = ExxGeo<SPLIT>::THREADS;
-  extern __shared__ __align__(16) uint64_t se[];  // [SPLIT ? 1 : 2][NP][M + N]
-  __shared__ uint4 soff[EXX_ROWS][NP];            // byte offsets of the four reads within a power
+  extern __shared__ __align__(16) uint64_t se[];  // [SPLIT ? 1 : 2][NP][M + N] difference arrays
+  __shared__ uint2 soff[EXX_ROWS][NP];            // byte offsets x0 = i d, x1 = i d + N (mod M)
+  __shared__ int srow_c[EXX_ROWS], scv[EXX_ROWS], sncv;
+  __shared__ uint32_t ssh[NP];
   const int N = rc.N, M = rc.M, n1 = rc.n1, L = M + N;
   const int rblocks = (N + EXX_ROWS - 1) / EXX_ROWS;
   const int j = (int)(blockIdx.x / rblocks), rb = (int)(blockIdx.x % rblocks);
@@ -231,45 +234,62 @@ __global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(con
   const uint64_t cu = a.cu;
   for (int t = threadIdx.x; t < nrows * NP; t += EX_THREADS) {
     const int r = t / NP, q = t - r * NP;
-    const uint32_t d = a.exps[q];
-    const uint32_t id = fastmod((uint32_t)(i0 + r) * d, M, rc.magicM);
-    const uint32_t sh = fastmod((uint32_t)(a.cvec[i0 + r] * n1) * d, M, rc.magicM);
+    const uint32_t id = fastmod((uint32_t)(i0 + r) * a.exps[q], M, rc.magicM);
     const uint32_t x1 = id + (uint32_t)N >= (uint32_t)M ? id + N - M : id + N;
-    soff[r][q] = make_uint4(8 * id, 8 * (id >= sh ? id - sh : id + M - sh), 8 * x1,
-                            8 * (x1 >= sh ? x1 - sh : x1 + M - sh));
+    soff[r][q] = make_uint2(8 * (q * L + id), 8 * (q * L + x1));
   }
-  const char* sb = reinterpret_cast<const char*>(se);
-#pragma unroll 1
-  for (int part = 0; part < (SPLIT ? 2 : 1); ++part) {
-    if (SPLIT && part) __syncthreads();  // every thread is done with component 0
-    // staged layout: [comp (SPLIT: only this part's)][q][L]
-    const int ncomp = SPLIT ? 1 : 2;
-    for (int idx = threadIdx.x; idx < ncomp * NP * L; idx += EX_THREADS) {
-      const int cq = idx / L, x = idx - cq * L;
-      const int comp = SPLIT ? part : cq / NP, q = cq - (cq / NP) * NP;
-      const int xm = x >= M ? x - M : x;
-      se[idx] = xm < N ? src[((int64_t)q * 2 + comp) * N + xm] * cu : 0ull;
+  for (int r = threadIdx.x; r < nrows; r += EX_THREADS) srow_c[r] = a.cvec[i0 + r];
+  __syncthreads();
+  if (threadIdx.x == 0) {  // distinct c_i of the tile (c_i is constant over runs of n1 rows)
+    int n = 0;
+    for (int r = 0; r < nrows; ++r) {
+      bool seen = false;
+      for (int u = 0; u < n; ++u) seen |= scv[u] == srow_c[r];
+      if (!seen) scv[n++] = srow_c[r];
     }
-    __syncthreads();
-    const int lane0 = SPLIT ? part * N : 0, lane1 = SPLIT ? lane0 + N : 2 * N;
-    for (int lane = lane0 + threadIdx.x; lane < lane1; lane += EX_THREADS) {
-      const int comp = lane >= N;
-      const int k = lane - comp * N;
-      const int kf = (int)fastmod((uint32_t)k, n1, rc.magicN1);
-      const char* ek = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + k);
-      const char* ef = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + kf);
-      uint64_t* dst = a.rows + g0 * 2 * N + lane;
+    sncv = n;
+  }
+  __syncthreads();
+  const char* sb = reinterpret_cast<const char*>(se);
+  const int ncv = sncv;
+#pragma unroll 1
+  for (int ci = 0; ci < ncv; ++ci) {
+    const int c = scv[ci];
+#pragma unroll 1
+    for (int part = 0; part < (SPLIT ? 2 : 1); ++part) {
+      if (threadIdx.x < NP) ssh[threadIdx.x] = fastmod((uint32_t)(c * n1) * a.exps[threadIdx.x], M, rc.magicM);
+      __syncthreads();  // shifts visible; every thread is done with the previous staging
+      // staged layout [comp (SPLIT: this part's only)][q][L]: D[x] = cu (ct[x mod M] - ct[(x - sh_q) mod M])
+      const int ncomp = SPLIT ? 1 : 2;
+      for (int idx = threadIdx.x; idx < ncomp * NP * L; idx += EX_THREADS) {
+        const int cq = idx / L, x = idx - cq * L;
+        const int comp = SPLIT ? part : cq / NP, q = cq - (cq / NP) * NP;
+        const uint32_t xm = x >= M ? x - M : x, sh = ssh[q];
+        const uint32_t y = xm >= sh ? xm - sh : xm + M - sh;
+        const uint64_t* s = src + ((int64_t)q * 2 + comp) * N;
+        const uint64_t v = (xm < (uint32_t)N ? s[xm] : 0ull) - (y < (uint32_t)N ? s[y] : 0ull);
+        se[idx] = v * cu;
+      }
+      __syncthreads();
+      const int lane0 = SPLIT ? part * N : 0, lane1 = SPLIT ? lane0 + N : 2 * N;
+      for (int lane = lane0 + threadIdx.x; lane < lane1; lane += EX_THREADS) {
+        const int comp = lane >= N;
+        const int k = lane - comp * N;
+        const int kf = (int)fastmod((uint32_t)k, n1, rc.magicN1);
+        const char* ek = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + k);
+        const char* ef = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + kf);
+        uint64_t* dst = a.rows + g0 * 2 * N + lane;
 #pragma unroll 4
-      for (int r = 0; r < nrows; ++r) {
-        uint64_t acc = 0;
+        for (int r = 0; r < nrows; ++r) {
+          if (srow_c[r] != c) continue;
+          uint64_t acc = 0;
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-          const uint4 o = soff[r][q];
-          const int qo = 8 * q * L;
-          acc += (*reinterpret_cast<const uint64_t*>(ek + qo + o.x) - *reinterpret_cast<const uint64_t*>(ek + qo + o.y)) -
-                 (*reinterpret_cast<const uint64_t*>(ef + qo + o.z) - *reinterpret_cast<const uint64_t*>(ef + qo + o.w));
+          for (int q = 0; q < NP; ++q) {
+            const uint2 o = soff[r][q];
+            acc += *reinterpret_cast<const uint64_t*>(ek + o.x) - *reinterpret_cast<const uint64_t*>(ef + o.y);
+          }
+          dst[(int64_t)r * 2 * N] = acc & QMASK;
         }
-        dst[(int64_t)r * 2 * N] = acc & QMASK;
       }
     }
   }
