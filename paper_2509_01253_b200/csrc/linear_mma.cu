@@ -42,7 +42,11 @@ constexpr int KC = 64;                    // taps per pipeline stage (2 MMAs)
 #endif
 constexpr int NSTAGE = SFHR_MMA_NSTAGE;  // pipeline depth (bytes in flight bound the gather rate)
 constexpr int STAGE_BYTES = KC * 128;     // 8 KB of A per stage
-constexpr int B_RESIDENT_MAX = 96 * 1024; // larger weight operands are streamed with each stage
+#ifndef SFHR_B_RESIDENT_KB
+#define SFHR_B_RESIDENT_KB 168  // A/B on B200 (linear ms per inference): ResNet-18 14.41 at 96 KB, 14.01 at 168; ResNet-34 343 -> 329
+#endif
+constexpr int B_RESIDENT_MAX = SFHR_B_RESIDENT_KB * 1024;  // larger weight operands are streamed with each stage
+constexpr int MMA_SMEM_CAP = 226 * 1024;                  // per-CTA carve-up limit (227 KB opt-in)
 constexpr int EP_COLS = 16;               // accumulator columns per epilogue chunk
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -144,9 +148,15 @@ __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_
 struct MmaSmem {
   int ring, stage, bstage, b, ep, colp, odst, obias, bars, tslot, total;
   bool stream;  // B streamed per stage (stage = A 8 KB + B chunk Np x 64 B) instead of resident
+  // B resident when it is at most B_RESIDENT_MAX and the whole carve-up fits MMA_SMEM_CAP
   __host__ __device__ static MmaSmem make(int Np, int Kp) {
+    MmaSmem r = layout(Np, Kp, false);
+    if (Np * Kp > B_RESIDENT_MAX || r.total > MMA_SMEM_CAP) r = layout(Np, Kp, true);
+    return r;
+  }
+  __host__ __device__ static MmaSmem layout(int Np, int Kp, bool stream) {
     MmaSmem s;
-    s.stream = Np * Kp > B_RESIDENT_MAX;
+    s.stream = stream;
     s.ring = 0;
     s.bstage = s.stream ? Np * KC : 0;
     s.stage = STAGE_BYTES + s.bstage;  // multiple of 1024 (Np % 16 == 0)
@@ -406,9 +416,10 @@ __global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_co
 size_t linear_mma_smem_bytes(int Np, int Kp) {
   // worst case over the tiles of a launch (N_pad <= Np, K_pad <= Kp): the streamed layout of
   // (Np, Kp) and any resident layout (B <= B_RESIDENT_MAX) with the same colp / row tables
-  const MmaSmem s = MmaSmem::make(Np, Kp);
+  const MmaSmem s = MmaSmem::layout(Np, Kp, true);
   const size_t bres = (size_t)Np * Kp < (size_t)B_RESIDENT_MAX ? (size_t)Np * Kp : (size_t)B_RESIDENT_MAX;
-  const size_t resident = (size_t)NSTAGE * STAGE_BYTES + ((bres + 127) & ~(size_t)127) + (s.total - s.ep);
+  size_t resident = (size_t)NSTAGE * STAGE_BYTES + ((bres + 127) & ~(size_t)127) + (s.total - s.ep);
+  if (resident > (size_t)MMA_SMEM_CAP) resident = MMA_SMEM_CAP;  // larger resident layouts stream
   return s.total > resident ? (size_t)s.total : resident;
 }
 
