@@ -317,10 +317,14 @@ class ServerEngine:
 
     def _run_round(self, state, session_id: bytes, round_no: int, power, exps):
         keys = self.clients[state.key_id]
-        in_map, out_map = self.round_maps(state, session_id, round_no)
-        im = torch.from_numpy(in_map).to(self.dev, non_blocking=True)
-        om = None if out_map is None else torch.from_numpy(out_map).to(self.dev, non_blocking=True)
-        packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, im, om)
+
+        def maps():
+            in_map, out_map = self.round_maps(state, session_id, round_no)
+            im = torch.from_numpy(in_map).to(self.dev, non_blocking=True)
+            om = None if out_map is None else torch.from_numpy(out_map).to(self.dev, non_blocking=True)
+            return im, om
+
+        packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, maps, None)
         state.next_round += 1
         state.last_seen = time.monotonic()
         if round_no == len(self.model.rounds):
@@ -389,7 +393,8 @@ class ServerEngine:
     def round_device(self, round_no: int, key: DeviceKey, power, exps, in_map, out_map,
                      timed: bool = True, groups: Optional[tuple] = None, counter=None):
         """Device part of one round. power: host (k, npow, 2, N) uint64 or device tensor;
-        in_map / out_map: device int64 tensors (out_map None for the final round).
+        in_map / out_map: device int64 tensors (out_map None for the final round), or
+        in_map a callable returning both, called once the extraction is launched.
 
         groups=(g0, g1) packs only that range of pack groups (multi-GPU sharding,
         SURVEY §8(e)); extraction and the linear map are computed in full.
@@ -406,6 +411,8 @@ class ServerEngine:
             ev[0].record(stream)
         pw = power if isinstance(power, torch.Tensor) else to_dev(power, self.dev)
         rows = extract_device(ctx, pw, exps, rnd.input_len)
+        if callable(in_map):  # lazy maps: derived / uploaded while the extraction runs
+            in_map, out_map = in_map()
         if ev:
             ev[1].record(stream)
         G = -(-rnd.output_len // F)
