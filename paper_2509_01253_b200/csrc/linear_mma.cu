@@ -31,11 +31,11 @@ namespace sfhr {
 namespace {
 
 constexpr int EPI_WARPS = 4;              // TMEM lanes 0-127
-#ifndef SFHR_MMA_PRODUCERS
-#define SFHR_MMA_PRODUCERS 128
-#endif
-constexpr int PRODUCERS = SFHR_MMA_PRODUCERS;  // cp.async gather threads
-constexpr int MMA_THREADS = EPI_WARPS * 32 + PRODUCERS + 32;
+// cp.async gather threads per CTA: a template parameter, chosen per launch from the widest tile
+// (A/B on B200, linear ms per inference: ResNet-20 (N <= 64, up to 4 CTAs/SM) 7.4 with 128 vs 8.0
+// with 256; ResNet-18 (N up to 256, 1-2 CTAs/SM by TMEM) 14.0 with 128 vs 12.7 with 256)
+template <int PRODUCERS>
+constexpr int mma_threads() { return EPI_WARPS * 32 + PRODUCERS + 32; }
 constexpr int KC = 64;                    // taps per pipeline stage (2 MMAs)
 #ifndef SFHR_MMA_NSTAGE
 #define SFHR_MMA_NSTAGE 4
@@ -172,9 +172,11 @@ struct MmaSmem {
   }
 };
 
-// Warp roles: 0-3 epilogue (TMEM lanes 32w..32w+31), 4-7 producers (cp.async
-// gathers, one mbarrier arrival per thread per stage), 8 MMA issuer.
-__global__ void __launch_bounds__(MMA_THREADS) linear_mma_kernel(const __grid_constant__ LinearMmaArgs a) {
+// Warp roles: 0-3 epilogue (TMEM lanes 32w..32w+31), then PRODUCERS / 32 producer warps
+// (cp.async gathers, one mbarrier arrival per thread per stage), then the MMA issuer.
+template <int PRODUCERS>
+__global__ void __launch_bounds__(mma_threads<PRODUCERS>()) linear_mma_kernel(const __grid_constant__ LinearMmaArgs a) {
+  constexpr int MMA_THREADS = mma_threads<PRODUCERS>();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tg = (int)(blockIdx.x % a.T);
@@ -433,13 +435,18 @@ cudaError_t launch_linear_mma(const LinearMmaArgs& a, int max_np, int max_kp, cu
   const size_t floor_bytes = (size_t)(228 * 1024) / (size_t)(512 / ncols + 1) + 1024;
   if (smem < floor_bytes) smem = floor_bytes;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(linear_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = max_np >= 128
+                      ? cudaFuncSetAttribute(linear_mma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                      : cudaFuncSetAttribute(linear_mma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t n_mt = (a.lanes + 15) / 16;
   const int64_t chunks = (n_mt + a.mt_per_cta - 1) / a.mt_per_cta;
   const int64_t grid = chunks * a.T;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
-  linear_mma_kernel<<<(unsigned)grid, MMA_THREADS, smem, st>>>(a);
+  if (max_np >= 128)
+    linear_mma_kernel<256><<<(unsigned)grid, mma_threads<256>(), smem, st>>>(a);
+  else
+    linear_mma_kernel<128><<<(unsigned)grid, mma_threads<128>(), smem, st>>>(a);
   return cudaGetLastError();
 }
 
