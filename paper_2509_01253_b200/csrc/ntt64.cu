@@ -212,8 +212,13 @@ __device__ __forceinline__ void inv_local(double* sm, int64_t c0, int s0, const 
         const int64_t k0 = ((int64_t)1 << s) + (B0 >> (logD + 1 - u));
         load_twiddles(1 << u, tw[h] + (1 << u) - 1, w + k0);
       }
+      // GS stages double X: a pass of >= 3 stages reduces after its second and stores values
+      // below ~1.6p, so two more stages from there stay below ~5p < 2^53 without reducing on load
 #pragma unroll
-      for (int lo = 0; lo < (1 << r); ++lo) v[h * (1 << r) + lo] = red_d(sm[pad(base[h] + lo * inner)], p, pinv);
+      for (int lo = 0; lo < (1 << r); ++lo) {
+        const double x = sm[pad(base[h] + lo * inner)];
+        v[h * (1 << r) + lo] = r <= 2 ? red_d(x, p, pinv) : x;
+      }
     }
 #pragma unroll
     for (int st = 0; st < r; ++st) {
