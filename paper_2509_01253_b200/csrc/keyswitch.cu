@@ -196,6 +196,10 @@ __device__ __forceinline__ void fwd_first_step(uint32_t* buf, int nb, const Ring
   __syncthreads();
 }
 
+// mid-stage work order: item-major (one item's index math for all digit buffers) for t <= 5
+template <int T>
+constexpr bool kItemMajor = T <= 5;
+
 // forward DIF stages s = 0 .. alpha-3 (all but the last, span > 1)
 template <int T, int A, int PR>
 __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const RingConst& rc,
@@ -208,12 +212,7 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
     if (!A && s >= g.alpha - 2) break;
     const int L = A ? cpow(T, A - 2 - s) : nsub / cpow(T, s);
     const int step = g.M / (T * L);
-    for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
-      const int q = w / g.nitems, it = w - q * g.nitems;
-      const int sub = it / nsub, rem = it - sub * nsub;
-      const int b = rem / L, j = rem - b * L;
-      uint32_t* v = buf + q * g.N + sub * g.n1 + b * T * L + j;
-      const int e1 = step * j;
+    auto item = [&](uint32_t* v, int e1) {
       uint32_t x[T], y[T];
 #pragma unroll
       for (int m = 0; m < T; ++m) x[m] = v[m * L];
@@ -221,6 +220,24 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
       v[0] = y[0];
 #pragma unroll
       for (int k = 1; k < T; ++k) v[k * L] = mont_mul(y[k], wt[e1 * k], pc.p, pc.pinv);
+    };
+    if constexpr (kItemMajor<T>) {
+      // item-major, buffers inner: position and twiddle exponent computed once for all nb
+      // transforms (A/B on B200: t = 5 stage kernel -6 %; t = 7 +3 %, so t = 7 stays flat)
+      for (int it = threadIdx.x; it < g.nitems; it += blockDim.x) {
+        const int sub = it / nsub, rem = it - sub * nsub;
+        const int b = rem / L, j = rem - b * L;
+        const int off = sub * g.n1 + b * T * L + j;
+#pragma unroll 1
+        for (int q = 0; q < nb; ++q) item(buf + q * g.N + off, step * j);
+      }
+    } else {
+      for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
+        const int q = w / g.nitems, it = w - q * g.nitems;
+        const int sub = it / nsub, rem = it - sub * nsub;
+        const int b = rem / L, j = rem - b * L;
+        item(buf + q * g.N + sub * g.n1 + b * T * L + j, step * j);
+      }
     }
     __syncthreads();
   }
@@ -238,12 +255,7 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
     if (!A && si >= g.alpha - 2) break;
     const int L = cpow(T, si + 1);
     const int step = g.M / (T * L);
-    for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
-      const int q = w / g.nitems, it = w - q * g.nitems;
-      const int sub = it / nsub, rem = it - sub * nsub;
-      const int b = rem / L, j = rem - b * L;
-      uint32_t* v = buf + q * g.N + sub * g.n1 + b * T * L + j;
-      const int e1 = step * j;
+    auto item = [&](uint32_t* v, int e1) {
       uint32_t z[T], x[T];
       z[0] = v[0];
 #pragma unroll
@@ -251,6 +263,22 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
       dft_inv_red<T>(z, x, pc);
 #pragma unroll
       for (int m = 0; m < T; ++m) v[m * L] = x[m];
+    };
+    if constexpr (kItemMajor<T>) {
+      for (int it = threadIdx.x; it < g.nitems; it += blockDim.x) {
+        const int sub = it / nsub, rem = it - sub * nsub;
+        const int b = rem / L, j = rem - b * L;
+        const int off = sub * g.n1 + b * T * L + j;
+#pragma unroll 1
+        for (int q = 0; q < nb; ++q) item(buf + q * g.N + off, step * j);
+      }
+    } else {
+      for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
+        const int q = w / g.nitems, it = w - q * g.nitems;
+        const int sub = it / nsub, rem = it - sub * nsub;
+        const int b = rem / L, j = rem - b * L;
+        item(buf + q * g.N + sub * g.n1 + b * T * L + j, step * j);
+      }
     }
     __syncthreads();
   }
