@@ -292,13 +292,19 @@ class ServerEngine:
         out_map = None if rnd.final else self._perm(state, session_id, round_no, rnd.output_len)
         return in_map, out_map
 
-    def _to_host_pinned(self, t: torch.Tensor) -> np.ndarray:
-        """Device -> host through a grow-only pinned staging buffer (one DMA, one memcpy)."""
+    def _stage_to_host(self, t: torch.Tensor) -> torch.Tensor:
+        """Enqueue device -> grow-only pinned staging buffer (valid after the next sync)."""
         n = t.numel()
         if getattr(self, "_pinned_out", None) is None or self._pinned_out.numel() < n:
             self._pinned_out = torch.empty(max(n, 1 << 17), dtype=torch.int64, pin_memory=True)
         stage = self._pinned_out[:n].view(t.shape)
-        stage.copy_(t)
+        stage.copy_(t, non_blocking=True)
+        return stage
+
+    def _to_host_pinned(self, t: torch.Tensor) -> np.ndarray:
+        """Device -> host through the pinned staging buffer (one DMA, one memcpy)."""
+        stage = self._stage_to_host(t)
+        torch.cuda.current_stream(self.dev).synchronize()
         return stage.numpy().view(np.uint64).copy()
 
     def _check_round(self, session_id: bytes, round_no: int, n_chunks: int):
@@ -315,7 +321,7 @@ class ServerEngine:
             raise ProtocolError(ERR_MALFORMED, f"expected {k_expected} chunks, got {n_chunks}")
         return state
 
-    def _run_round(self, state, session_id: bytes, round_no: int, power, exps):
+    def _run_round(self, state, session_id: bytes, round_no: int, power, exps, fetch=None):
         keys = self.clients[state.key_id]
 
         def maps():
@@ -324,7 +330,7 @@ class ServerEngine:
             om = None if out_map is None else torch.from_numpy(out_map).to(self.dev, non_blocking=True)
             return im, om
 
-        packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, maps, None)
+        packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, maps, None, fetch=fetch)
         state.next_round += 1
         state.last_seen = time.monotonic()
         if round_no == len(self.model.rounds):
@@ -343,8 +349,10 @@ class ServerEngine:
         """Reference ServerEngine.server_round (protocol.py:219-280): bundles in, packed cts out."""
         state = self._check_round(session_id, round_no, len(bundles))
         power, exps = self._upload_bundles(bundles)
-        packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps)
-        packs_host = self._to_host_pinned(packs_dev)
+        staged = []  # packs are copied to pinned memory before the round's single sync
+        packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps,
+                                                fetch=lambda p: staged.append(self._stage_to_host(p)))
+        packs_host = staged[0].numpy().view(np.uint64).copy()
         packed = [packs_host[i] for i in range(packs_host.shape[0])]
         if self.extra_noise_std > 0:
             q = float(1 << 53)
@@ -391,7 +399,7 @@ class ServerEngine:
         return packed, self._stats(nks, times, int(power.shape[0]), len(packed))
 
     def round_device(self, round_no: int, key: DeviceKey, power, exps, in_map, out_map,
-                     timed: bool = True, groups: Optional[tuple] = None, counter=None):
+                     timed: bool = True, groups: Optional[tuple] = None, counter=None, fetch=None):
         """Device part of one round. power: host (k, npow, 2, N) uint64 or device tensor;
         in_map / out_map: device int64 tensors (out_map None for the final round), or
         in_map a callable returning both, called once the extraction is launched.
@@ -400,6 +408,7 @@ class ServerEngine:
         SURVEY §8(e)); extraction and the linear map are computed in full.
         counter: optional device int64 accumulator; when given the call does not
         synchronise and returns key_switches=None (the caller reads the counter).
+        fetch: optional callable run on the packs after the last launch, before the sync.
         Returns (packs_dev, key_switches, (extract_s, linear_s, pack_s)).
         """
         rnd = self.model.rounds[round_no - 1]
@@ -427,6 +436,8 @@ class ServerEngine:
         packs = pack_device(ctx, key, buf[g0 * F:g1 * F], g1 - g0, cnt, skip_zero=True)
         if ev:
             ev[3].record(stream)
+        if fetch is not None:  # e.g. enqueue the D2H of the packs ahead of the sync below
+            fetch(packs)
         if counter is not None:
             return packs, None, (0.0, 0.0, 0.0)
         nks = int(cnt.item())  # synchronises the stream
