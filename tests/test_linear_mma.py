@@ -45,6 +45,7 @@ PASSES = {
     "resnet20_r7": lambda: mm.lower_round(W.resnet20_model(12, 0), 7),
     "resnet20_fc": lambda: mm.lower_round(W.resnet20_model(12, 0), 19),
     "toy": lambda: mm.lower_round(W.toy_model(8, 3), 0),
+    "toy_pool": lambda: mm.lower_round(W.toy_model(8, 3), 2),  # per-row (pooling) groups as tiles
     "mlp": lambda: mm.lower_round(W.mlp_model(0), 0),
     "dense_wide": lambda: [lin._dense_pass(np.random.default_rng(5).integers(-127, 128, (300, 45)))],
     "dense_big_w": lambda: [lin._dense_pass(np.random.default_rng(6).integers(-500, 500, (20, 8)))],
