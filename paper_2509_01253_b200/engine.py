@@ -349,10 +349,18 @@ class ServerEngine:
         """Reference ServerEngine.server_round (protocol.py:219-280): bundles in, packed cts out."""
         state = self._check_round(session_id, round_no, len(bundles))
         power, exps = self._upload_bundles(bundles)
-        staged = []  # packs are copied to pinned memory before the round's single sync
-        packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps,
-                                                fetch=lambda p: staged.append(self._stage_to_host(p)))
-        packs_host = staged[0].numpy().view(np.uint64).copy()
+        # packs are copied into a fresh pinned block (torch's caching host allocator, so no
+        # cudaHostAlloc per round) before the round's single sync; the returned arrays are
+        # views that keep the block alive, so there is no host-side copy
+        staged = []
+
+        def fetch(p):
+            host = torch.empty(p.shape, dtype=p.dtype, pin_memory=True)
+            host.copy_(p, non_blocking=True)
+            staged.append(host)
+
+        packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps, fetch=fetch)
+        packs_host = staged[0].numpy().view(np.uint64)
         packed = [packs_host[i] for i in range(packs_host.shape[0])]
         if self.extra_noise_std > 0:
             q = float(1 << 53)
