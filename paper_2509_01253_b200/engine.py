@@ -270,8 +270,11 @@ class ServerEngine:
         if getattr(self, "_pinned", None) is None or self._pinned.numel() < n:
             self._pinned = torch.empty(n, dtype=torch.int64, pin_memory=True)
         host = self._pinned[:n].numpy().view(np.uint64).reshape(shape)
+        need = {}  # power_exponents per gamma, computed once per call
         for j, b in enumerate(bundles):
-            if set(b.power_cts) != set(exps) or set(exps) != set(power_exponents(b.gamma, R)):
+            if b.gamma not in need:
+                need[b.gamma] = set(power_exponents(b.gamma, R))
+            if set(b.power_cts) != set(exps) or set(exps) != need[b.gamma]:
                 raise ValueError(f"bundle exponents {sorted(b.power_cts)} != required "
                                  f"{sorted(power_exponents(self.scheme.gamma, R))}")
             for q, d in enumerate(exps):
