@@ -431,10 +431,10 @@ class ServerEngine:
             ev[0].record(stream)
         pw = power if isinstance(power, torch.Tensor) else to_dev(power, self.dev)
         rows = extract_device(ctx, pw, exps, rnd.input_len)
-        if callable(in_map):  # lazy maps: derived / uploaded while the extraction runs
-            in_map, out_map = in_map()
         if ev:
             ev[1].record(stream)
+        if callable(in_map):  # lazy maps: derived / uploaded while the extraction runs
+            in_map, out_map = in_map()
         G = -(-rnd.output_len // F)
         buf = torch.empty((G * F, 2, ctx.N), dtype=torch.int64, device=self.dev)
         if G * F > rnd.output_len:
