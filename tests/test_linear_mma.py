@@ -154,3 +154,35 @@ def test_mma_round_matches_cuda_core_kernel(net, r, monkeypatch):
         torch.cuda.synchronize()
         outs.append(out.cpu().numpy())
     assert np.array_equal(outs[0], outs[2]) and np.array_equal(outs[1], outs[2])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("run_rows,same_rows", [(16, 16), (128, 128), (256, 256)])
+def test_tiler_knobs_do_not_change_results(run_rows, same_rows, monkeypatch):
+    """Any tile-group merging (pixel runs, shared-list runs) gives the CUDA-core result."""
+    import torch
+    from paper_2509_01253_b200.device import RingContext
+    from paper_2509_01253_b200.params import preset_for_bits
+    model = W.resnet20_model(12, 0)
+    sch = preset_for_bits(12, 0)
+    R = sch.ring
+    ctx = RingContext.get(R.t, R.alpha, R.p_bits, sch.gadget.D, sch.gadget.l, 0, sch.beta, 0)
+    r = 2  # 16-channel 3x3 conv with a residual extra
+    rnd = model.rounds[r]
+    rng = np.random.default_rng(77)
+    x = torch.from_numpy(rng.integers(0, 1 << 53, (rnd.input_len, 2, R.N), dtype=np.uint64).view(np.int64)).cuda()
+    in_map = torch.from_numpy(rng.permutation(rnd.input_len).astype(np.int64)).cuda()
+    unit = torch.from_numpy(rng.integers(0, 1 << 53, R.N, dtype=np.uint64).view(np.int64)).cuda()
+    passes = mm.lower_round(model, r)
+    outs = []
+    for knobs in ((run_rows, same_rows, True), (64, 256, False)):
+        monkeypatch.setattr(lin, "MMA_RUN_ROWS", knobs[0])
+        monkeypatch.setattr(lin, "MMA_SAME_ROWS", knobs[1])
+        monkeypatch.setattr(lin, "MMA_ENABLED", knobs[2])
+        dps = [lin.DevicePass(p, ctx.dev) for p in passes]
+        out = torch.zeros((rnd.output_len, 2, R.N), dtype=torch.int64, device=ctx.dev)
+        lin.run_round(ctx, dps, x, in_map, out, None, unit)
+        torch.cuda.synchronize()
+        outs.append(out.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
