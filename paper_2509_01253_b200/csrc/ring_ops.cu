@@ -207,7 +207,7 @@ constexpr int EXX_MAXPOW = 6;
 #define SFHR_EXX_ROWS 16
 #endif
 constexpr int EXX_ROWS = SFHR_EXX_ROWS;  // rows per CTA (A/B on B200: 16 > 8 > 32)
-constexpr size_t EXX_SMEM_MAX = 227 * 1024;
+constexpr size_t EXX_SMEM_MAX = 220 * 1024;  // dynamic part; static tables (<= 7 KB) take the rest of 227 KB
 
 // SPLIT kernels hold one CTA per SM: twice the threads and 4x the rows per staging of the powers
 template <bool SPLIT> struct ExxGeo {
