@@ -279,9 +279,7 @@ __global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(con
         const char* ek = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + k);
         const char* ef = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + kf);
         uint64_t* dst = a.rows + g0 * 2 * N + lane;
-#pragma unroll 4
-        for (int r = 0; r < nrows; ++r) {
-          if (srow_c[r] != c) continue;
+        auto row = [&](int r) {
           uint64_t acc = 0;
 #pragma unroll
           for (int q = 0; q < NP; ++q) {
@@ -289,6 +287,14 @@ __global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(con
             acc += *reinterpret_cast<const uint64_t*>(ek + o.x) - *reinterpret_cast<const uint64_t*>(ef + o.y);
           }
           dst[(int64_t)r * 2 * N] = acc & QMASK;
+        };
+        if (ncv == 1) {  // the common case: one c_i for the whole tile, no per-row test
+#pragma unroll 4
+          for (int r = 0; r < nrows; ++r) row(r);
+        } else {
+#pragma unroll 4
+          for (int r = 0; r < nrows; ++r)
+            if (srow_c[r] == c) row(r);
         }
       }
     }
