@@ -48,15 +48,20 @@ __global__ void merge_kernel(const __grid_constant__ RingConst rc, const uint64_
   const int r = (int)(orow - g * rest);
   const int N = rc.N, M = rc.M;
   const int nm = MEM ? MEM : members;
+  const int st = (int)((uint32_t)stride % (uint32_t)M);  // member a rotates by a * st (mod M)
   for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < N; k += gridDim.y * blockDim.x) {
     const int km = (int)fastmod((uint32_t)k, rc.n1, rc.magicN1);
     uint64_t t1[MEM ? MEM : 1], t2[MEM ? MEM : 1];
     uint64_t acc = 0;
     // all members' loads are issued before any is consumed (MEM is the compile-time count)
+    int e = 0;
 #pragma unroll
     for (int a = 0; a < (MEM ? MEM : 1); ++a) {
       const uint64_t* v = in + ((g * nm + a) * (int64_t)rest + r) * 2 * N + (int64_t)comp * N;
-      const int e = (int)(((int64_t)a * stride) % M);
+      if (a) {
+        e += st;
+        if (e >= M) e -= M;
+      }
       int s1 = k - e;
       if (s1 < 0) s1 += M;
       int s2 = N + km - e;
