@@ -214,10 +214,13 @@ constexpr int EXX_MAXPOW = 6;
 constexpr int EXX_ROWS = SFHR_EXX_ROWS;  // rows per CTA (A/B on B200: 16 > 8 > 32)
 constexpr size_t EXX_SMEM_MAX = 220 * 1024;  // dynamic part; static tables (<= 7 KB) take the rest of 227 KB
 
-// SPLIT kernels hold one CTA per SM: twice the threads and 4x the rows per staging of the powers
+// SPLIT kernels hold one CTA per SM: twice the threads and more rows per staging of the powers
 template <bool SPLIT> struct ExxGeo {
   static constexpr int THREADS = SPLIT ? 1024 : EX_THREADS;
-  static constexpr int ROWS = SPLIT ? 4 * EXX_ROWS : EXX_ROWS;
+#ifndef SFHR_EXX_SPLIT_MULT
+#define SFHR_EXX_SPLIT_MULT 2  // A/B (ResNet-18 extraction ms): 16 rows 6.34, 32 rows 5.48, 64 rows 5.67, 128 rows 7.13
+#endif
+  static constexpr int ROWS = SPLIT ? SFHR_EXX_SPLIT_MULT * EXX_ROWS : EXX_ROWS;
 };
 
 template <int NP, bool SPLIT>
