@@ -135,6 +135,10 @@ typedef struct {
 int sfhr_linear_pass(sfhr_ctx* ctx, const sfhr_linear_desc* desc, void* stream);
 /* sizeof(sfhr_linear_desc), for binding-layout checks */
 size_t sfhr_linear_desc_bytes(void);
+/* Largest s8 weight operand (bytes, N_pad * K_pad) the tensor-core linear kernel keeps
+ * resident in shared memory; larger tile groups stream their weights per pipeline stage.
+ * The host tiler (linear.split_mma_tiles) merges groups only below this size. */
+size_t sfhr_mma_b_resident_bytes(void);
 
 /* ServerEngine._pack / tracepack.pack_rows + fast_pack (reference
  * protocol.py:296-321, tracepack.py:288-348) for n_groups zero-padded groups

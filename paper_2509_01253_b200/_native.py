@@ -49,6 +49,7 @@ def _load() -> C.CDLL:
         "sfhr_pack": (i32, [vp, vp, vp, i64, vp, vp, sz, i32, vp, vp]),
         "sfhr_derive_permutation": (i32, [vp, i32, vp, i32, u32, i64, vp]),
         "sfhr_last_error": (C.c_char_p, []),
+        "sfhr_mma_b_resident_bytes": (sz, []),
         "sfhr_launch_count": (C.c_ulonglong, []),
         "sfhr_profile_enable": (i32, [vp, i32]),
         "sfhr_profile_collect": (i32, [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong),

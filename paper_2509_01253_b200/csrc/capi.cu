@@ -286,6 +286,7 @@ int sfhr_ctx_debug_tables(const sfhr_ctx* ctx, void* ringconst, size_t rc_bytes,
 size_t sfhr_ringconst_bytes(void) { return sizeof(RingConst); }
 
 size_t sfhr_linear_desc_bytes(void) { return sizeof(sfhr_linear_desc); }
+size_t sfhr_mma_b_resident_bytes(void) { return sfhr::linear_mma_b_resident_bytes(); }
 
 int sfhr_ctx_dual(const sfhr_ctx* ctx, int32_t* e1, int32_t* e2, int32_t* ratio_len) {
   if (!ctx) return fail(SFHR_EINVAL, "null context");

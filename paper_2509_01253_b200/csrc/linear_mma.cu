@@ -415,6 +415,8 @@ __global__ void __launch_bounds__(mma_threads<PRODUCERS>()) linear_mma_kernel(co
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols) : "memory");
 }
 
+size_t linear_mma_b_resident_bytes() { return (size_t)B_RESIDENT_MAX; }
+
 size_t linear_mma_smem_bytes(int Np, int Kp) {
   // worst case over the tiles of a launch (N_pad <= Np, K_pad <= Kp): the streamed layout of
   // (Np, Kp) and any resident layout (B <= B_RESIDENT_MAX) with the same colp / row tables

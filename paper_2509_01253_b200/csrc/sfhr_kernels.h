@@ -101,6 +101,7 @@ struct LinearMmaArgs {
   int mt_per_cta;            // 128-byte M-tiles per CTA
 };
 size_t linear_mma_smem_bytes(int Np, int Kp);
+size_t linear_mma_b_resident_bytes();
 cudaError_t launch_linear_mma(const LinearMmaArgs& a, int max_np, int max_kp, cudaStream_t st);
 
 }  // namespace sfhr

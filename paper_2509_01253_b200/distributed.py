@@ -67,36 +67,34 @@ class DistributedServerEngine:
         return self.engine.open_session(session_id, key_id)
 
     def server_round(self, session_id: bytes, round_no: int, bundles):
-        from .engine import RoundStats, round_req_size, round_resp_size
+        """ServerEngine.server_round semantics (protocol checks, session state, extra
+        noise, counters; reference protocol.py:219-280) with the pack groups sharded."""
         from .device import to_host_u64
         eng = self.engine
-        state = eng.sessions.get(session_id)
-        if state is None:
-            from .engine import ERR_BAD_SESSION, ProtocolError
-            raise ProtocolError(ERR_BAD_SESSION, "unknown or expired session")
-        rnd = eng.model.rounds[round_no - 1]
-        F = eng.scheme.pack_factor
-        G = -(-rnd.output_len // F)
-        power, exps = eng._upload_bundles(bundles)
-        in_map, out_map = eng.round_maps(state, session_id, round_no)
-        im = torch.from_numpy(in_map).to(eng.dev)
-        om = None if out_map is None else torch.from_numpy(out_map).to(eng.dev)
-        g0, g1 = group_range(G, self.rank, self.world)
-        key = eng.clients[state.key_id].key
-        local, nks, times = eng.round_device(round_no, key, power, exps, im, om, groups=(g0, g1))
-        full = gather_packs(local, G, self.world, self.group)
-        cnt = torch.tensor([nks], dtype=torch.int64, device=eng.dev)
-        dist.all_reduce(cnt, group=self.group)
-        state.next_round += 1
-        if round_no == len(eng.model.rounds):
-            eng.sessions.pop(session_id, None)
-        host = to_host_u64(full)
-        packed = [host[i] for i in range(G)]
-        st = RoundStats(extract_s=times[0], linear_s=times[1], pack_s=times[2],
-                        key_switches=int(cnt.item()), packed_coefficients=G * F,
-                        bytes_up=round_req_size(eng.scheme, len(bundles)),
-                        bytes_down=round_resp_size(eng.scheme, G))
-        return packed, st
+        with eng._lock:
+            state = eng._check_round(session_id, round_no, len(bundles))
+            rnd = eng.model.rounds[round_no - 1]
+            F = eng.scheme.pack_factor
+            G = -(-rnd.output_len // F)
+            power, exps = eng._upload_bundles(bundles)
+            eng._prefetch_perms(state, session_id, round_no + 1)
+            in_map, out_map = eng.round_maps(state, session_id, round_no)
+            im = torch.from_numpy(in_map).to(eng.dev)
+            om = None if out_map is None else torch.from_numpy(out_map).to(eng.dev)
+            g0, g1 = group_range(G, self.rank, self.world)
+            key = eng.clients[state.key_id].key
+            local, nks, times = eng.round_device(round_no, key, power, exps, im, om, groups=(g0, g1))
+            full = gather_packs(local, G, self.world, self.group)
+            cnt = torch.tensor([nks], dtype=torch.int64, device=local.device)
+            dist.all_reduce(cnt, group=self.group)
+            total = int(cnt.item())
+            eng._finish_round(session_id, state, round_no, total)
+            host = to_host_u64(full)
+            packed = [host[i] for i in range(G)]
+            # every rank's noise generator is seeded from the same master seed and advanced by
+            # the same calls, so the noisy packs agree across ranks
+            eng._apply_extra_noise(packed)
+            return packed, eng._stats(total, times, len(bundles), G)
 
 
 def _selftest_assemble(world: int, n_groups: int) -> np.ndarray:

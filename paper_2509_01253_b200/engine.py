@@ -15,12 +15,13 @@ Per round, on the device (one stream, no host round trips in between):
   4. fast packing of all pack groups, level-synchronous (merge + fused
      key-switch stage kernels)
   5. D2H of the packed ciphertexts and the live key-switch count.
-sigma_r comes from the C++ port of derive_permutation and is computed for
-the whole session on a host thread when the session opens.
+sigma_r comes from the C++ port of derive_permutation; round r+1's permutations
+are derived on a host thread while round r runs on the GPU.
 """
 
 from __future__ import annotations
 
+import concurrent.futures
 import functools
 import hashlib
 import json
@@ -140,7 +141,7 @@ class _SessionState:
     key_id: bytes
     next_round: int = 1
     last_seen: float = field(default_factory=time.monotonic)
-    perms: object = None   # dict[(round, size)] -> Future[np.ndarray]
+    perms: dict = field(default_factory=dict)   # (round, size) -> Future[np.ndarray]
 
 
 @dataclass
@@ -161,6 +162,8 @@ def _serialized(fn):
 
 class ServerEngine:
     """Holds the model and per-client key material; executes server rounds on a B200."""
+
+    MAX_QUEUED_PERMS = 64  # engine-wide cap on prefetched permutation derivations
 
     def __init__(self, model: QuantModel, scheme: SchemeParams, master_seed: bytes = b"\x00" * 32,
                  threads: int = 1, shuffle_enabled: bool = True, ks_mode: str = "cuda",
@@ -193,6 +196,7 @@ class ServerEngine:
         self._passes = [[DevicePass(p, self.dev) for p in lower_round(model, r)]
                         for r in range(len(model.rounds))]
         self._perm_pool = ThreadPoolExecutor(max_workers=4)
+        self._pending: list = []  # queued / running permutation derivations (all sessions)
         # The reference serves one TCP connection per thread (transport.py:136-156), so
         # calls on different sessions may be concurrent; they share this engine's device
         # buffers, pinned staging and stream, so they run one at a time.
@@ -213,25 +217,41 @@ class ServerEngine:
             self.clients[key_id] = _ClientKeys(ksk=ksk, key=DeviceKey(self.ctx, ksk), scheme=self.scheme)
         return key_id
 
-    def _perm_schedule(self, session_id: bytes) -> dict:
-        """Futures of all permutations a session will use, keyed by (round_no, size).
+    def _round_perm_keys(self, round_no: int) -> list:
+        """(round, size) keys of the permutations round round_no consumes (protocol.py:243-263)."""
+        if not 1 <= round_no <= len(self.model.rounds):
+            return []
+        rnd = self.model.rounds[round_no - 1]
+        keys = [(round_no - 1, rnd.input_len - rnd.skip_len)]
+        if rnd.skip_len:
+            keys.append((rnd.skip_source + 1, rnd.skip_len))
+        if not rnd.final:
+            keys.append((round_no, rnd.output_len))
+        return keys
 
-        Submitted in the order the rounds consume them, so round r waits only for
-        its own sigma_{r-1} / sigma_r while later ones are derived (C++, GIL released)
-        on the pool's other threads during the GPU work of the earlier rounds."""
-        need = []
-        for r, rnd in enumerate(self.model.rounds, start=1):
-            main = rnd.input_len - rnd.skip_len
-            need.append((r - 1, main))
-            if rnd.skip_len:
-                need.append((rnd.skip_source + 1, rnd.skip_len))
-            if not rnd.final:
-                need.append((r, rnd.output_len))
-        out = {}
-        for key in need:
-            if key not in out:
-                out[key] = self._perm_pool.submit(self._perm_now, session_id, *key)
-        return out
+    def _prefetch_perms(self, state: _SessionState, session_id: bytes, round_no: int):
+        """Queue the derivations of round round_no's permutations on the pool (C++, GIL
+        released), so they run while the current round is on the GPU.
+
+        Only one round ahead is prefetched per session (the reference derives each
+        permutation lazily when its round runs, protocol.py:212-217), and nothing is
+        queued once the engine already has MAX_QUEUED_PERMS derivations pending: a burst
+        of opened or abandoned sessions cannot make later rounds wait behind them."""
+        for key in self._round_perm_keys(round_no):
+            if key in state.perms:
+                continue
+            self._pending = [f for f in self._pending if not f.done()]
+            if len(self._pending) >= self.MAX_QUEUED_PERMS:
+                return  # derived lazily by _perm when the round needs it
+            fut = self._perm_pool.submit(self._perm_now, session_id, *key)
+            self._pending.append(fut)
+            state.perms[key] = fut
+
+    @staticmethod
+    def _cancel_perms(state: _SessionState):
+        for fut in state.perms.values():
+            fut.cancel()
+        state.perms.clear()
 
     def _perm_now(self, session_id, round_no, size):
         if not self.shuffle_enabled or round_no == 0:
@@ -246,37 +266,61 @@ class ServerEngine:
         if session_id in self.sessions:
             raise ProtocolError(ERR_BAD_SESSION, "session id already in use")
         st = _SessionState(key_id=key_id)
-        st.perms = self._perm_schedule(session_id)
         self.sessions[session_id] = st
+        self._prefetch_perms(st, session_id, 1)
         return metadata_for(self.model, self.scheme)
 
     def _reap(self):
         now = time.monotonic()
         for sid in [s for s, st in self.sessions.items() if now - st.last_seen > self.session_timeout]:
-            del self.sessions[sid]
+            self._cancel_perms(self.sessions.pop(sid))
 
     def _perm(self, state: _SessionState, session_id: bytes, round_no: int, size: int) -> np.ndarray:
-        fut = state.perms.get((round_no, size)) if state.perms is not None else None
-        return fut.result() if fut is not None else self._perm_now(session_id, round_no, size)
+        fut = state.perms.get((round_no, size))
+        if fut is None or fut.cancelled():
+            fut = concurrent.futures.Future()
+            fut.set_result(self._perm_now(session_id, round_no, size))
+            state.perms[(round_no, size)] = fut  # sigma_r is used again by round r+1 (unshuffle)
+        return fut.result()
+
+    def _finish_round(self, session_id: bytes, state: _SessionState, round_no: int, nks: int):
+        """Session bookkeeping after a round (reference protocol.py:265-270)."""
+        state.next_round += 1
+        state.last_seen = time.monotonic()
+        if round_no == len(self.model.rounds):
+            self._cancel_perms(state)
+            self.sessions.pop(session_id, None)
+        else:  # keep only the permutations a later round still consumes (residual skips reach back)
+            later = {k for q in range(round_no + 1, len(self.model.rounds) + 1) for k in self._round_perm_keys(q)}
+            for k in [k for k in state.perms if k not in later]:
+                state.perms.pop(k).cancel()
+        self.total_key_switches += nks
 
     # -- round processing ------------------------------------------------------
+
+    def _check_bundle_exponents(self, gammas, exps_per_bundle):
+        """One rule for both entry points: every bundle must carry the engine's extraction
+        level (the bias unit and the pack schedule are built for scheme.gamma; the
+        reference checks each bundle against its own gamma only, tracepack.py:108-111,
+        and would then combine mismatched rows) and exactly its power exponents."""
+        want = sorted(power_exponents(self.scheme.gamma, self.scheme.ring))
+        for g, exps in zip(gammas, exps_per_bundle):
+            if g != self.scheme.gamma:
+                raise ProtocolError(ERR_MALFORMED, f"bundle gamma {g} != engine gamma {self.scheme.gamma}")
+            if list(exps) != want:
+                raise ValueError(f"bundle exponents {list(exps)} != required {want}")
 
     def _upload_bundles(self, bundles):
         """Stage the uploads in pinned host memory and copy them to the device."""
         R = self.scheme.ring
         exps = sorted(bundles[0].power_cts)
+        self._check_bundle_exponents([b.gamma for b in bundles], [sorted(b.power_cts) for b in bundles])
         shape = (len(bundles), len(exps), 2, R.N)
         n = int(np.prod(shape))
         if getattr(self, "_pinned", None) is None or self._pinned.numel() < n:
             self._pinned = torch.empty(n, dtype=torch.int64, pin_memory=True)
         host = self._pinned[:n].numpy().view(np.uint64).reshape(shape)
-        need = {}  # power_exponents per gamma, computed once per call
         for j, b in enumerate(bundles):
-            if b.gamma not in need:
-                need[b.gamma] = set(power_exponents(b.gamma, R))
-            if set(b.power_cts) != set(exps) or set(exps) != need[b.gamma]:
-                raise ValueError(f"bundle exponents {sorted(b.power_cts)} != required "
-                                 f"{sorted(power_exponents(self.scheme.gamma, R))}")
             for q, d in enumerate(exps):
                 ct = b.power_cts[d]
                 host[j, q, 0] = ct.a
@@ -333,12 +377,9 @@ class ServerEngine:
             om = None if out_map is None else torch.from_numpy(out_map).to(self.dev, non_blocking=True)
             return im, om
 
+        self._prefetch_perms(state, session_id, round_no + 1)  # derived while this round runs
         packs_dev, nks, times = self.round_device(round_no, keys.key, power, exps, maps, None, fetch=fetch)
-        state.next_round += 1
-        state.last_seen = time.monotonic()
-        if round_no == len(self.model.rounds):
-            self.sessions.pop(session_id, None)
-        self.total_key_switches += nks
+        self._finish_round(session_id, state, round_no, nks)
         return packs_dev, nks, times
 
     def _stats(self, nks, times, n_chunks, n_packs):
@@ -365,12 +406,17 @@ class ServerEngine:
         packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps, fetch=fetch)
         packs_host = staged[0].numpy().view(np.uint64)
         packed = [packs_host[i] for i in range(packs_host.shape[0])]
-        if self.extra_noise_std > 0:
-            q = float(1 << 53)
-            for pk in packed:
-                extra = np.rint(self._noise_rng.normal(0.0, self.extra_noise_std, pk.shape[-1]) * q)
-                pk[1] = (pk[1] + extra.astype(np.int64).astype(np.uint64)) & np.uint64((1 << 53) - 1)
+        self._apply_extra_noise(packed)
         return packed, self._stats(nks, times, len(bundles), len(packed))
+
+    def _apply_extra_noise(self, packed):
+        """Optional host-side extra noise on the packed bodies (reference protocol.py:314-320)."""
+        if self.extra_noise_std <= 0:
+            return
+        q = float(1 << 53)
+        for pk in packed:
+            extra = np.rint(self._noise_rng.normal(0.0, self.extra_noise_std, pk.shape[-1]) * q)
+            pk[1] = (pk[1] + extra.astype(np.int64).astype(np.uint64)) & np.uint64((1 << 53) - 1)
 
     @_serialized
     def server_round_wire(self, session_id: bytes, round_no: int, payload) -> tuple:
@@ -388,9 +434,10 @@ class ServerEngine:
         except WireError as e:
             raise ProtocolError(ERR_MALFORMED, e.reason) from e
         state = self._check_round(session_id, round_no, int(power.shape[0]))
-        want = sorted(power_exponents(self.scheme.gamma, R))
-        if exps != want or any(g != self.scheme.gamma for g in gammas):
-            raise ProtocolError(ERR_MALFORMED, f"bundle exponents {exps} != required {want}")
+        try:
+            self._check_bundle_exponents(gammas, [exps] * len(gammas))
+        except ValueError as e:
+            raise ProtocolError(ERR_MALFORMED, str(e)) from e
         if self.extra_noise_std > 0:
             packed, st = self._round_from_device_with_noise(state, session_id, round_no, power, exps)
             noisy = torch.from_numpy(np.stack(packed).view(np.int64)).to(self.dev)
@@ -403,10 +450,7 @@ class ServerEngine:
         packs_dev, nks, times = self._run_round(state, session_id, round_no, power, exps)
         packs_host = to_host_u64(packs_dev)
         packed = [packs_host[i] for i in range(packs_host.shape[0])]
-        q = float(1 << 53)
-        for pk in packed:
-            extra = np.rint(self._noise_rng.normal(0.0, self.extra_noise_std, pk.shape[-1]) * q)
-            pk[1] = (pk[1] + extra.astype(np.int64).astype(np.uint64)) & np.uint64((1 << 53) - 1)
+        self._apply_extra_noise(packed)
         return packed, self._stats(nks, times, int(power.shape[0]), len(packed))
 
     def round_device(self, round_no: int, key: DeviceKey, power, exps, in_map, out_map,

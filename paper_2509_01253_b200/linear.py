@@ -61,7 +61,10 @@ MMA_GATHER_CLK = float(os.environ.get("SFHR_MMA_GATHER_CLK", "6.5"))
 # inference: 9.44 unmerged, 7.64 at 64 rows / 2x2 pixel blocks, 8.5-10.9 at 96-256 rows)
 MMA_RUN_ROWS = int(os.environ.get("SFHR_MMA_RUN_ROWS", "64"))
 MMA_SAME_ROWS = int(os.environ.get("SFHR_MMA_SAME_ROWS", str(MMA_MAX_ROWS)))  # runs sharing one list
-MMA_B_RESIDENT = 96 * 1024  # csrc/linear_mma.cu B_RESIDENT_MAX
+# merged s8 weight operands stay at or below this size (A/B-tuned: larger merged tiles lose
+# more to zero-weight MACs than they save in gathers); it must not exceed what the kernel keeps
+# resident in shared memory (sfhr_mma_b_resident_bytes(), B_RESIDENT_MAX in csrc/linear_mma.cu)
+MMA_MERGE_B_MAX = min(96 * 1024, int(nat.lib.sfhr_mma_b_resident_bytes()))
 
 
 def _run_cost(k_pad: int, n_pad: int, rows: int) -> float:
@@ -75,8 +78,9 @@ def split_mma_tiles(ps: LinearPass):
     becomes one tile group over the union of their column lists (conv: the
     output-channel chunks of a pixel, then neighbouring pixels of the lowering's
     pixel blocks, whose 3x3 windows overlap; fc / dense: all row chunks) while
-    the cost model above improves, N <= 256 and the s8 weights stay resident in
-    shared memory.  Runs with |w| > 127 stay on the CUDA-core kernel; per-row column
+    the cost model above improves, N <= 256 and the merged s8 weights stay within
+    MMA_MERGE_B_MAX (<= the kernel's resident-weight limit, so merged runs never stream
+    their weights; unmerged wide layers above it do).  Runs with |w| > 127 stay on the CUDA-core kernel; per-row column
     lists (pooling, identity) join as block-sparse tile groups over the union of their
     rows' columns.
     """
@@ -119,7 +123,7 @@ def split_mma_tiles(ps: LinearPass):
                 break
             u2 = union if same else np.union1d(union, gcols(j))
             k2, n2 = (len(u2) + 31) // 32 * 32, (tot + nrj + 15) // 16 * 16
-            if k2 > MMA_MAX_KPAD or (n2 * k2 > MMA_B_RESIDENT and not same):
+            if k2 > MMA_MAX_KPAD or (n2 * k2 > MMA_MERGE_B_MAX and not same):
                 break
             c2 = _run_cost(k2, n2, tot + nrj)
             if not same and c2 > 0.98 * best:

@@ -138,3 +138,53 @@ def test_mlp_exact_logits_end_to_end(gamma):
     x = mlp_input(0)
     logits, _ = _client_inference(model, 16, gamma, 1, x)
     assert logits.tolist() == olo.cleartext_forward(model, x).tolist()
+
+
+def test_distributed_engine_matches_server_round():
+    """DistributedServerEngine (NCCL, one rank) == ServerEngine.server_round on the same
+    uploads, with the same protocol checks, session state and extra noise."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_2509_01253_b200.distributed import DistributedServerEngine
+    from paper_2509_01253_b200.engine import ERR_STALE_ROUND, ProtocolError, ServerEngine
+    from paper_2509_01253_b200.keyswitch import KeySwitchKeySet, RlweCiphertext
+    from paper_2509_01253_b200.tracepack import PowerBundle
+    from paper_2509_01253_b200.workloads import mlp_model
+    sch = osc.preset(16, 1)
+    R, g, mys = _mine(sch)
+    model = mlp_model(0)
+    keys = _uniform_keys(sch, 8)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        engs = [ServerEngine(model, mys, master_seed=bytes(range(32)), extra_noise_std=2.0 ** -40)
+                for _ in range(2)]
+        kids = [e.register_client(KeySwitchKeySet(keys, g, 0.0, R)) for e in engs]
+        sid = bytes(range(16))
+        for e, kid in zip(engs, kids):
+            e.open_session(sid, kid)
+        de = DistributedServerEngine(engs[1])
+        exps = opk.power_exponents(1, sch.ring)
+        rng = np.random.default_rng(21)
+        with pytest.raises(ProtocolError) as ei:
+            de.server_round(sid, 2, [])
+        assert ei.value.code == ERR_STALE_ROUND
+        for rno, rnd in enumerate(model.rounds, start=1):
+            k = -(-rnd.input_len // R.N)
+            power = rng.integers(0, 1 << 53, (k, len(exps), 2, R.N), dtype=np.uint64)
+            bundles = [PowerBundle(1, {d: RlweCiphertext(power[j, q, 0], power[j, q, 1])
+                                       for q, d in enumerate(exps)}) for j in range(k)]
+            want, st_w = engs[0].server_round(sid, rno, bundles)
+            got, st_g = de.server_round(sid, rno, bundles)
+            assert np.array_equal(np.stack(got), np.stack(want))
+            assert st_g.key_switches == st_w.key_switches
+        assert sid not in engs[1].sessions
+        assert engs[1].total_key_switches == engs[0].total_key_switches
+    finally:
+        dist.destroy_process_group()
