@@ -157,6 +157,19 @@ int sfhr_pack(sfhr_ctx* ctx, const sfhr_key* key, uint64_t* rows, int64_t n_grou
 int sfhr_derive_permutation(const uint8_t* master_seed, int seed_len, const uint8_t* session_id,
                             int sid_len, uint32_t round_no, int64_t size, int64_t* out);
 
+/* Tensor-core forward key switch (keyswitch_tc.cu; ring row t = 7, l in {2, 3}): the
+ * constant operands the library builds for each CRT prime (planning-only contexts too),
+ * for host-side verification against tests/tc_model.py.  tabs: sfhr_tc_table_bytes()
+ * bytes; old_idx: 42 * 49 int32.  sfhr_ctx_set_tc(ctx, k): stage launches with >= k switched
+ * representatives use the tensor-core forward (k = 0: never, i.e. the CUDA-core forward of
+ * ks_stage_kernel everywhere, the default: measured faster on B200); SFHR_TC_MIN_REPS=k sets
+ * the default of new contexts.
+ * sfhr_ctx_tc_enabled returns the current k. */
+size_t sfhr_tc_table_bytes(const sfhr_ctx* ctx);
+int sfhr_ctx_tc_tables(const sfhr_ctx* ctx, uint8_t* tabs, size_t tab_bytes, int32_t* old_idx);
+int sfhr_ctx_tc_enabled(const sfhr_ctx* ctx);
+int sfhr_ctx_set_tc(sfhr_ctx* ctx, int enable);
+
 const char* sfhr_last_error(void);
 
 /* Number of CUDA kernels this library has launched (process-wide counter). */

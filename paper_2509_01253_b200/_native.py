@@ -50,6 +50,10 @@ def _load() -> C.CDLL:
         "sfhr_derive_permutation": (i32, [vp, i32, vp, i32, u32, i64, vp]),
         "sfhr_last_error": (C.c_char_p, []),
         "sfhr_mma_b_resident_bytes": (sz, []),
+        "sfhr_tc_table_bytes": (sz, [vp]),
+        "sfhr_ctx_tc_tables": (i32, [vp, vp, sz, vp]),
+        "sfhr_ctx_tc_enabled": (i32, [vp]),
+        "sfhr_ctx_set_tc": (i32, [vp, i32]),
         "sfhr_launch_count": (C.c_ulonglong, []),
         "sfhr_profile_enable": (i32, [vp, i32]),
         "sfhr_profile_collect": (i32, [vp, C.POINTER(C.c_double), C.POINTER(C.c_longlong),

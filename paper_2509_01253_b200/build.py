@@ -20,13 +20,13 @@ INCLUDE = ROOT / "include"
 OBJ = PKG / "_build"
 LIB = PKG / "libsfhr_b200.so"
 
-SOURCES = ["keyswitch.cu", "ring_ops.cu", "linear_mma.cu", "ntt64.cu", "wire.cu", "capi.cu", "plan.cpp", "perm.cpp"]
+SOURCES = ["keyswitch.cu", "keyswitch_tc.cu", "ring_ops.cu", "linear_mma.cu", "ntt64.cu", "wire.cu", "capi.cu", "plan.cpp", "perm.cpp"]
 # (object name, source, extra -D flags): the stage-kernel template fan-out is
 # split into one translation unit per (t, l) so it compiles in parallel
 UNITS = [(s, s, []) for s in SOURCES] + [
     (f"keyswitch_t{t}_l{l}.cu", "keyswitch.cu", [f"-DSFHR_KS_T={t}", f"-DSFHR_KS_L={l}"])
     for t in (3, 5, 7) for l in (1, 2, 3, 4, 5)]
-HEADERS = ["sfhr_common.cuh", "sfhr_kernels.h", "plan.h"]
+HEADERS = ["sfhr_common.cuh", "sfhr_kernels.h", "plan.h", "tc_ptx.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]

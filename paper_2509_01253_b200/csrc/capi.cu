@@ -38,6 +38,15 @@ struct sfhr_ctx {
   std::vector<cudaEvent_t> ev_pool;  // recycled events
   uint32_t* twid = nullptr;  // [np][twid_stride(M)]
   int32_t* cvec = nullptr;   // [N]
+  // tensor-core forward key switch (keyswitch_tc.cu): constant operands per prime and the
+  // NTT-order map; null when the ring row has no tensor-core path or SFHR_TC=0
+  uint8_t* tc_tabs = nullptr;
+  int32_t* tc_oldidx = nullptr;
+  int tc_min_reps = 0;       // stage launches with >= this many switched reps take the tensor-core
+                             // path (0: never; sfhr_ctx_set_tc)
+  uint32_t* tc_ws = nullptr;  // NTT-domain accumulator workspace (grow-only), last used on ...
+  size_t tc_ws_bytes = 0;
+  cudaEvent_t tc_ws_free = nullptr;  // ... the stream position recorded here
   std::mutex mu;
 };
 
@@ -46,6 +55,7 @@ struct sfhr_key {
   std::map<uint32_t, int> slot;  // d -> slot
   uint32_t* spectra = nullptr;   // [nidx][l][2][np][N]
   size_t slot_words = 0;
+  uint2* tc_keys = nullptr;      // [nidx][l][np][49][42] tensor-core MAC operands (tc path only)
 };
 
 namespace {
@@ -111,6 +121,25 @@ int key_slot(const sfhr_key* key, uint32_t d) {
   return it->second;
 }
 
+int64_t tc_chunk_rows() {
+  static const int64_t rows = [] {
+    const char* e = std::getenv("SFHR_TC_CHUNK");
+    const long long v = e ? std::atoll(e) : 0;
+    return (int64_t)(v > 0 ? v : 2048);
+  }();
+  return rows;
+}
+
+// The tensor-core forward (keyswitch_tc.cu) is bit-exact but measured slower than the CUDA-core
+// forward on B200 (ResNet-20 stage kernel 132 -> 141 ms with it on 6-rep stages,
+// 24 -> 32 ms at gamma = 1), so it is opt-in: SFHR_TC_MIN_REPS=k (or sfhr_ctx_set_tc) routes
+// stage launches with >= k switched representatives through it.
+int tc_default_min_reps() {
+  const char* e = std::getenv("SFHR_TC_MIN_REPS");
+  const int v = e ? std::atoi(e) : 0;
+  return v > 0 ? v : 0;
+}
+
 int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nreps, int identity,
               const uint64_t* in, uint64_t* out, int64_t B, int skip_zero,
               unsigned long long* counter, cudaStream_t st) {
@@ -156,7 +185,77 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     if (in != out) CK(cudaMemcpyAsync(out, in, (size_t)B * 2 * P.rc.N * 8, cudaMemcpyDeviceToDevice, st), "stage copy");
     return SFHR_OK;
   }
-  CK(launch_stage(P.rc, a, st), "stage kernel");
+  if (ctx->tc_min_reps > 0 && ctx->tc_tabs && key->tc_keys && ns >= ctx->tc_min_reps) {
+    // tensor-core forward (NTT-domain accumulators) + the CUDA-core kernel's inverse / CRT tail,
+    // in chunks whose accumulators (49 KB per row at b = 12) stay L2-sized
+    TcFwdArgs f;
+    std::memset(&f, 0, sizeof(f));
+    f.nreps = ns;
+    f.tabs = ctx->tc_tabs;
+    f.old_idx = ctx->tc_oldidx;
+    f.off = tc_digit_offset(P.rc);
+    for (int r = 0; r < ns; ++r) {
+      f.dinv[r] = a.dinv[r];
+      f.keys[r] = key->tc_keys + (size_t)(a.spec[r] - key->spectra) / key->slot_words *
+                                     (tc_keys_bytes(P.rc, 1) / sizeof(uint2));
+    }
+    const int64_t chunk = tc_chunk_rows();
+    const size_t acc_bytes = (size_t)std::min<int64_t>(B, chunk) * P.rc.np * 2 * P.rc.N * 4;
+    if (!ctx->tc_ws_free) CK(cudaEventCreateWithFlags(&ctx->tc_ws_free, cudaEventDisableTiming), "tc event");
+    if (acc_bytes > ctx->tc_ws_bytes) {  // grow (rare): wait for the last user before freeing
+      CK(cudaEventSynchronize(ctx->tc_ws_free), "tc workspace sync");
+      cudaFree(ctx->tc_ws);
+      ctx->tc_ws = nullptr;
+      ctx->tc_ws_bytes = 0;
+      CK(cudaMalloc(reinterpret_cast<void**>(&ctx->tc_ws), acc_bytes), "tc accumulator alloc");
+      ctx->tc_ws_bytes = acc_bytes;
+    }
+    CK(cudaStreamWaitEvent(st, ctx->tc_ws_free, 0), "tc workspace wait");  // a previous caller's stream
+    uint32_t* acc = ctx->tc_ws;
+    for (int64_t r0 = 0; r0 < B; r0 += chunk) {
+      const int64_t nb = std::min<int64_t>(chunk, B - r0);
+      f.in = in + r0 * 2 * P.rc.N;
+      f.B = nb;
+      f.acc = acc;
+      static const bool tc_trace = std::getenv("SFHR_TC_TRACE") != nullptr;
+      std::vector<long long> trace_host;
+      if (tc_trace) {
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&f.trace), 4 * TC_TRACE_N * 8, st), "trace alloc");
+        CK(cudaMemsetAsync(f.trace, 0, 4 * TC_TRACE_N * 8, st), "trace memset");
+      }
+      CK(launch_tc_fwd(P.rc, f, st), "tensor-core key-switch kernel");
+      if (tc_trace) {  // debug timeline of CTA 0 (SFHR_TC_TRACE=1), one line per role
+        trace_host.resize(4 * TC_TRACE_N);
+        CK(cudaMemcpyAsync(trace_host.data(), f.trace, trace_host.size() * 8, cudaMemcpyDeviceToHost, st), "trace copy");
+        CK(cudaStreamSynchronize(st), "trace sync");
+        CK(cudaFree(f.trace), "trace free");
+        f.trace = nullptr;
+        long long t0 = trace_host[0];
+        for (long long v : trace_host) if (v && v < t0) t0 = v;
+        std::fprintf(stderr, "[tc-trace] B=%lld nreps=%d\n", (long long)nb, ns);
+        for (int role = 0; role < 4; ++role) {
+          std::fprintf(stderr, "[tc-trace] role %d:", role);
+          for (int k = 0; k < TC_TRACE_N; ++k) {
+            const long long v = trace_host[role * TC_TRACE_N + k];
+            if (!v) break;
+            std::fprintf(stderr, " %lld", v - t0);
+          }
+          std::fprintf(stderr, "\n");
+        }
+      }
+      StageArgs t = a;
+      t.in = in + r0 * 2 * P.rc.N;
+      t.out = out + r0 * 2 * P.rc.N;
+      t.B = nb;
+      t.acc_in = acc;
+      CK(launch_stage(P.rc, t, st), "stage kernel (inverse / CRT)");
+      g_launches += 2;
+    }
+    CK(cudaEventRecord(ctx->tc_ws_free, st), "tc workspace release");
+    --g_launches;  // counted once below
+  } else {
+    CK(launch_stage(P.rc, a, st), "stage kernel");
+  }
   if (g_debug_sync) {  // SFHR_DEBUG_SYNC=1: locate a faulting launch
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
@@ -232,9 +331,22 @@ int sfhr_ctx_create(int t, int alpha, int p_bits, int D, int l, int gamma, int b
   if (e == cudaSuccess) e = cudaMemcpy(ctx->twid, P.twid.data(), P.twid.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->cvec, P.cvec.size() * 4);
   if (e == cudaSuccess) e = cudaMemcpy(ctx->cvec, P.cvec.data(), P.cvec.size() * 4, cudaMemcpyHostToDevice);
+  const char* tc_env = std::getenv("SFHR_TC");
+  ctx->tc_min_reps = tc_supported(P.rc) && !(tc_env && tc_env[0] == '0') ? tc_default_min_reps() : 0;
+  if (e == cudaSuccess && tc_supported(P.rc)) {
+    std::vector<uint8_t> tabs(tc_table_bytes(P.rc));
+    std::vector<int32_t> oi(42 * 49);
+    tc_build_tables(P.rc, P.twid.data(), twid_stride(P.rc.M), tabs.data(), oi.data());
+    e = cudaMalloc(&ctx->tc_tabs, tabs.size());
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->tc_tabs, tabs.data(), tabs.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->tc_oldidx, oi.size() * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->tc_oldidx, oi.data(), oi.size() * 4, cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     cudaFree(ctx->twid);
     cudaFree(ctx->cvec);
+    cudaFree(ctx->tc_tabs);
+    cudaFree(ctx->tc_oldidx);
     delete ctx;
     return cuda_fail(e, "ctx create");
   }
@@ -256,6 +368,11 @@ int sfhr_ctx_destroy(sfhr_ctx* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaFree(ctx->twid);
   cudaFree(ctx->cvec);
+  cudaFree(ctx->tc_tabs);
+  cudaFree(ctx->tc_oldidx);
+  if (ctx->tc_ws_free) cudaEventSynchronize(ctx->tc_ws_free);
+  cudaFree(ctx->tc_ws);
+  if (ctx->tc_ws_free) cudaEventDestroy(ctx->tc_ws_free);
   delete ctx;
   return SFHR_OK;
 }
@@ -280,6 +397,30 @@ int sfhr_ctx_debug_tables(const sfhr_ctx* ctx, void* ringconst, size_t rc_bytes,
   if (rc_bytes != sizeof(RingConst)) return fail(SFHR_EINVAL, "RingConst size mismatch");
   std::memcpy(ringconst, &P.rc, sizeof(RingConst));
   if (twid) std::memcpy(twid, P.twid.data(), std::min(twid_words, P.twid.size()) * 4);
+  return SFHR_OK;
+}
+
+int sfhr_ctx_tc_tables(const sfhr_ctx* ctx, uint8_t* tabs, size_t tab_bytes, int32_t* old_idx) {
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  const Plan& P = ctx->plan;
+  if (!tc_supported(P.rc)) return fail(SFHR_EINVAL, "ring row has no tensor-core key-switch path");
+  if (tab_bytes != tc_table_bytes(P.rc)) return fail(SFHR_EINVAL, "tensor-core table size mismatch");
+  tc_build_tables(P.rc, P.twid.data(), twid_stride(P.rc.M), tabs, old_idx);
+  return SFHR_OK;
+}
+
+size_t sfhr_tc_table_bytes(const sfhr_ctx* ctx) {
+  return ctx && tc_supported(ctx->plan.rc) ? tc_table_bytes(ctx->plan.rc) : 0;
+}
+
+int sfhr_ctx_tc_enabled(const sfhr_ctx* ctx) { return ctx && ctx->tc_tabs ? ctx->tc_min_reps : 0; }
+
+int sfhr_ctx_set_tc(sfhr_ctx* ctx, int min_reps) {
+  if (!ctx) return fail(SFHR_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (min_reps < 0) return fail(SFHR_EINVAL, "negative representative threshold");
+  if (min_reps && !ctx->tc_tabs) return fail(SFHR_EINVAL, "ring row has no tensor-core key-switch path");
+  ctx->tc_min_reps = min_reps;
   return SFHR_OK;
 }
 
@@ -329,8 +470,14 @@ int sfhr_register_ksk(sfhr_ctx* ctx, const uint32_t* idx, int nidx, const uint64
   a.twid = ctx->twid;
   e = launch_spectra(rc, a, nidx * rc.l * 2, (cudaStream_t)stream);
   if (nidx) ++g_launches;
+  if (e == cudaSuccess && ctx->tc_tabs && nidx > 0) {
+    e = cudaMalloc(&key->tc_keys, tc_keys_bytes(rc, nidx));
+    if (e == cudaSuccess) e = launch_tc_keys(rc, key->spectra, nidx, ctx->tc_oldidx, key->tc_keys, (cudaStream_t)stream);
+    if (e == cudaSuccess) ++g_launches;
+  }
   if (e != cudaSuccess) {
     cudaFree(key->spectra);
+    cudaFree(key->tc_keys);
     delete key;
     return cuda_fail(e, "ksk spectra kernel");
   }
@@ -342,6 +489,7 @@ int sfhr_key_destroy(sfhr_key* key) {
   if (!key) return SFHR_OK;
   DeviceGuard g(key->ctx->device);
   cudaFree(key->spectra);
+  cudaFree(key->tc_keys);
   delete key;
   return SFHR_OK;
 }

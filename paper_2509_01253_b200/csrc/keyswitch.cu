@@ -138,34 +138,6 @@ __device__ __forceinline__ void dft_inv_red(const uint32_t (&x)[T], uint32_t (&y
   else dft_t<T>(x, y, pc.zi, pc.p, pc.pinv);
 }
 
-// balanced base-D digits of y < 2^53 (reference crypto.py:288-323), all at once
-template <int L>
-__device__ __forceinline__ void decompose(uint64_t y, int (&dg)[L], const RingConst& rc) {
-  if (rc.dlog2 >= 0) {
-    const int w = rc.dlog2, D = rc.D;
-    uint64_t u = (y + (1ull << (rc.shift - 1))) >> rc.shift;
-    int carry = 0;
-#pragma unroll
-    for (int i = L - 1; i >= 0; --i) {
-      const int x = (int)(u & (uint64_t)(D - 1)) + carry;
-      u >>= w;
-      carry = x > (D >> 1);
-      dg[i] = carry ? x - D : x;
-    }
-  } else {
-    const long long D = rc.D;
-    long long r = (long long)y;
-    if (y > (1ull << 52)) r -= (1ll << 53);
-#pragma unroll
-    for (int i = 0; i < L; ++i) {
-      const long long prod = r * D;
-      const long long d = (prod + (1ll << 52)) >> 53;
-      dg[i] = (int)d;
-      r = prod - d * (1ll << 53);
-    }
-  }
-}
-
 __device__ __forceinline__ uint32_t lift_signed(int d, uint32_t p) {
   return d < 0 ? (uint32_t)(d + (int)p) : (uint32_t)d;
 }
@@ -383,7 +355,15 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   const int item = threadIdx.x;
   const bool owner = item < g.nitems;
 
-  for (int r = 0; r < a.nreps; ++r) {
+  if (a.acc_in) {
+    // NTT-domain accumulators come from the tensor-core forward kernel (keyswitch_tc.cu)
+    const uint4* src = reinterpret_cast<const uint4*>(a.acc_in + ((size_t)row * rc.np + PR) * 2 * N);
+    uint4* dst = reinterpret_cast<uint4*>(S.acc);
+    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) dst[c] = src[c];  // 2N u32 = N/2 uint4
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    __syncthreads();
+  }
+  for (int r = 0; r < (a.acc_in ? 0 : a.nreps); ++r) {
     const uint32_t dinv = a.dinv[r];
 #if SFHR_FUSED_FIRST_STEP
     // ---- A+B fused: per column m, gather the T-1 coefficients j*n1+m of

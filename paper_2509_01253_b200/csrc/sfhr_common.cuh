@@ -84,6 +84,34 @@ __device__ __forceinline__ uint32_t fastmod(uint32_t x, uint32_t M, uint32_t mag
   return r >= M ? r - M : r;
 }
 
+// balanced base-D digits of y < 2^53 (reference crypto.py:288-323), all at once
+template <int L>
+__device__ __forceinline__ void decompose(uint64_t y, int (&dg)[L], const RingConst& rc) {
+  if (rc.dlog2 >= 0) {
+    const int w = rc.dlog2, D = rc.D;
+    uint64_t u = (y + (1ull << (rc.shift - 1))) >> rc.shift;
+    int carry = 0;
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) {
+      const int x = (int)(u & (uint64_t)(D - 1)) + carry;
+      u >>= w;
+      carry = x > (D >> 1);
+      dg[i] = carry ? x - D : x;
+    }
+  } else {
+    const long long D = rc.D;
+    long long r = (long long)y;
+    if (y > (1ull << 52)) r -= (1ll << 53);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const long long prod = r * D;
+      const long long d = (prod + (1ll << 52)) >> 53;
+      dg[i] = (int)d;
+      r = prod - d * (1ll << 53);
+    }
+  }
+}
+
 #endif  // __CUDACC__
 
 }  // namespace sfhr

@@ -21,6 +21,10 @@ struct StageArgs {
   const uint32_t* spec[MAXREPS];  // key spectra of each rep: [l][2][np][N]
   const uint32_t* twid;   // [np][twid_stride(M)] omega^e * R mod p (e <= M)
   unsigned long long* counter;    // live-row switch counter (may be null)
+  // tensor-core forward path: NTT-domain accumulators already summed over reps and digits
+  // ([B][np][2][N] u32, old NTT order, any value < 2^32) -> the kernel only runs the
+  // inverse transforms, CRT and identity / body terms
+  const uint32_t* acc_in;
 };
 
 struct SpecArgs {
@@ -28,6 +32,32 @@ struct SpecArgs {
   uint32_t* out;          // (jobs, np, N) thread-owned layout
   const uint32_t* twid;
 };
+
+// tensor-core forward key switch (keyswitch_tc.cu), ring row t = 7, l in {2, 3}
+struct TcFwdArgs {
+  const uint64_t* in;           // (B, 2, N) rows
+  int64_t B;
+  int nreps;
+  uint32_t dinv[MAXREPS];       // as StageArgs
+  const uint2* keys[MAXREPS];   // per rep: [l][np][49][42] (Ka, Kb) = K^ R^2 mod p
+  const uint8_t* tabs;          // per prime constant operands (tc_table_bytes)
+  const int32_t* old_idx;       // [42][49] position of (o, k1) in the CUDA-core kernel's NTT order
+  uint32_t* acc;                // (B, np, 2, N) NTT-domain accumulators out
+  int off;                      // digit offset (tc_digit_offset)
+  int cpp;                      // CTAs per prime (set by the launcher)
+  long long* trace;             // debug (SFHR_TC_TRACE): CTA 0's role event clocks, [4 roles][TC_TRACE_N]
+};
+constexpr int TC_TRACE_N = 512;
+bool tc_supported(const RingConst& rc);
+size_t tc_table_bytes(const RingConst& rc);
+int tc_digit_offset(const RingConst& rc);
+void tc_build_tables(const RingConst& rc, const uint32_t* twid, int twid_stride_words, uint8_t* tabs,
+                     int32_t* old_idx);
+size_t tc_fwd_smem_bytes(int L);
+size_t tc_keys_bytes(const RingConst& rc, int nslots);
+cudaError_t launch_tc_fwd(const RingConst& rc, const TcFwdArgs& a, cudaStream_t st);
+cudaError_t launch_tc_keys(const RingConst& rc, const uint32_t* spectra, int nslots, const int32_t* old_idx,
+                           uint2* out, cudaStream_t st);
 
 size_t stage_smem_bytes(const RingConst& rc);
 int stage_threads(const RingConst& rc);

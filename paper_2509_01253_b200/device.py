@@ -85,6 +85,16 @@ class RingContext:
     def stream(self) -> int:
         return stream_ptr(self.dev)
 
+    @property
+    def tensor_core_min_reps(self) -> int:
+        """Stage launches with at least this many switched representatives use the
+        tensor-core forward key switch (keyswitch_tc.cu); 0 = never."""
+        return int(nat.lib.sfhr_ctx_tc_enabled(self.h))
+
+    @tensor_core_min_reps.setter
+    def tensor_core_min_reps(self, k: int) -> None:
+        nat.check(nat.lib.sfhr_ctx_set_tc(self.h, int(k)))
+
     def counter(self) -> torch.Tensor:
         return torch.zeros(1, dtype=torch.int64, device=self.dev)
 
