@@ -199,19 +199,25 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
       f.keys[r] = key->tc_keys + (size_t)(a.spec[r] - key->spectra) / key->slot_words *
                                      (tc_keys_bytes(P.rc, 1) / sizeof(uint2));
     }
-    const int64_t chunk = tc_chunk_rows();
+    // chunks: the operand tiles of a chunk (nreps * l * 6 KB per row) stay L2-sized
+    const int64_t per_row_tiles = (int64_t)tc_tile_bytes(P.rc, 2, ns) / 2;
+    int64_t chunk = std::min<int64_t>(tc_chunk_rows(), std::max<int64_t>(2, (64ll << 20) / per_row_tiles));
+    chunk &= ~1ll;
     const size_t acc_bytes = (size_t)std::min<int64_t>(B, chunk) * P.rc.np * 2 * P.rc.N * 4;
+    const size_t tile_bytes = tc_tile_bytes(P.rc, std::min<int64_t>(B, chunk), ns);
+    const size_t ws_bytes = ((acc_bytes + 1023) & ~(size_t)1023) + tile_bytes;
     if (!ctx->tc_ws_free) CK(cudaEventCreateWithFlags(&ctx->tc_ws_free, cudaEventDisableTiming), "tc event");
-    if (acc_bytes > ctx->tc_ws_bytes) {  // grow (rare): wait for the last user before freeing
+    if (ws_bytes > ctx->tc_ws_bytes) {  // grow (rare): wait for the last user before freeing
       CK(cudaEventSynchronize(ctx->tc_ws_free), "tc workspace sync");
       cudaFree(ctx->tc_ws);
       ctx->tc_ws = nullptr;
       ctx->tc_ws_bytes = 0;
-      CK(cudaMalloc(reinterpret_cast<void**>(&ctx->tc_ws), acc_bytes), "tc accumulator alloc");
-      ctx->tc_ws_bytes = acc_bytes;
+      CK(cudaMalloc(reinterpret_cast<void**>(&ctx->tc_ws), ws_bytes), "tc workspace alloc");
+      ctx->tc_ws_bytes = ws_bytes;
     }
     CK(cudaStreamWaitEvent(st, ctx->tc_ws_free, 0), "tc workspace wait");  // a previous caller's stream
     uint32_t* acc = ctx->tc_ws;
+    f.tiles = reinterpret_cast<unsigned char*>(ctx->tc_ws) + ((acc_bytes + 1023) & ~(size_t)1023);
     for (int64_t r0 = 0; r0 < B; r0 += chunk) {
       const int64_t nb = std::min<int64_t>(chunk, B - r0);
       f.in = in + r0 * 2 * P.rc.N;
@@ -249,10 +255,10 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
       t.B = nb;
       t.acc_in = acc;
       CK(launch_stage(P.rc, t, st), "stage kernel (inverse / CRT)");
-      g_launches += 2;
+      g_launches += 3;
     }
     CK(cudaEventRecord(ctx->tc_ws_free, st), "tc workspace release");
-    --g_launches;  // counted once below
+    --g_launches;  // counted once below (digits + tensor-core forward + inverse per chunk)
   } else {
     CK(launch_stage(P.rc, a, st), "stage kernel");
   }

@@ -61,17 +61,16 @@ constexpr int BB_BYTES = KB * NBH;     // 25088 per half
 constexpr int TWS = 43;                // twiddle table row stride (uint2), bank-conflict free
 constexpr int TW_BYTES = SB * TWS * 8; // 16856
 constexpr int TAB_BYTES = BA_BYTES + 2 * BB_BYTES + ((TW_BYTES + 15) & ~15);  // per prime
-constexpr int XA_BYTES = 2 * N * 8;    // both rows' mask components
-constexpr int UNITS = 2 * 6 * 7 * 13;  // producer work units per rep
+constexpr int XA_BYTES = 2 * N * 8;    // digits kernel: both rows' mask components
 constexpr int EB_WARPS = 16;           // E_B: 4 lane quadrants x 2 k1-halves x 2 parts ([0,12), [12,25|24))
-constexpr int EA_WARPS = 4;            // E_A: 4 lane quadrants
-constexpr int NPROD = 7;               // producer warps
-constexpr int PROD_WARP0 = EB_WARPS + EA_WARPS;
-constexpr int NTHREADS = (PROD_WARP0 + NPROD + 1) * 32;  // 28 warps: 7 per SMSP leaves 72 registers
+constexpr int EA_WARPS = 8;            // E_A: 4 lane quadrants x 2 output halves
+constexpr int LOAD_WARP = EB_WARPS + EA_WARPS;
+constexpr int MMA_WARP = LOAD_WARP + 1;
+constexpr int NTHREADS = (MMA_WARP + 1) * 32;  // 26 warps: 7 per SMSP leaves 72 registers
 // TMEM columns: pass A, the NTT-domain accumulators (a / b, k1-half h at +28h), pass-B halves
 constexpr uint32_t COL_A = 0, COL_ACC_A = 176, COL_ACC_B = 232, COL_B0 = 288, COL_B1 = 400;
-constexpr int NBARS = 16;
-constexpr int MMA_WARP = PROD_WARP0 + NPROD;
+constexpr int NBARS = 14;
+constexpr int DIG_THREADS = 256;       // digits kernel block
 
 // byte address of (K row k, M lane m) in an MN-major 128B-swizzled u8 operand tile
 __device__ __forceinline__ uint32_t swz(uint32_t tile, int k, int m) {
@@ -79,23 +78,22 @@ __device__ __forceinline__ uint32_t swz(uint32_t tile, int k, int m) {
 }
 
 struct Smem {
-  int aa, ab, ba, bb, tw, xa, bars, tslot, total;
+  int aa, ab, ba, bb, tw, bars, tslot, total;
   __host__ __device__ static Smem make(int L) {
     Smem s;
-    s.aa = 0;
-    s.ab = s.aa + L * AA_BYTES;
+    s.aa = 0;                          // two sets of L pass-A operand tiles (double-buffered reps)
+    s.ab = s.aa + 2 * L * AA_BYTES;
     s.ba = s.ab + 2 * AB_BYTES;
     s.bb = s.ba + BA_BYTES;
     s.tw = s.bb + 2 * BB_BYTES;
-    s.xa = s.tw + ((TW_BYTES + 15) & ~15);
-    s.bars = s.xa + XA_BYTES;
+    s.bars = s.tw + ((TW_BYTES + 15) & ~15);
     s.tslot = s.bars + NBARS * 8;
     s.total = s.tslot + 16 + 1024;  // + alignment slack for the 1024-B swizzle atoms
     return s;
   }
 };
 
-enum { XA_FULL0, XA_FULL1, XA_EMPTY0, XA_EMPTY1, AA_FULL, AA_EMPTY, TA_FULL, TA_EMPTY, AB_FULL0, AB_FULL1, AB_EMPTY0, AB_EMPTY1,
+enum { AA_FULL0, AA_FULL1, AA_EMPTY0, AA_EMPTY1, TA_FULL, TA_EMPTY, AB_FULL0, AB_FULL1, AB_EMPTY0, AB_EMPTY1,
        TB_FULL0, TB_FULL1, TB_EMPTY0, TB_EMPTY1 };
 
 // debug timeline (CTA 0 only): role 0 producers, 1 MMA, 2 E_A, 3 E_B; events appended in order
@@ -119,28 +117,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const Smem S = Smem::make(L);
   const uint32_t aa = su32(sm + S.aa), ab = su32(sm + S.ab), ba = su32(sm + S.ba), bb = su32(sm + S.bb);
   const uint2* tw = reinterpret_cast<const uint2*>(sm + S.tw);
-  const uint64_t* xa = reinterpret_cast<const uint64_t*>(sm + S.xa);
   const uint32_t bars = su32(sm + S.bars);
   auto bar = [&](int i) { return bars + 8u * (uint32_t)i; };
   uint32_t* tslot = reinterpret_cast<uint32_t*>(sm + S.tslot);
 
-  // ---- setup: constant operands of this prime, the ones row of every pass-A tile ----
+  // ---- setup: constant operands of this prime ----
   {
     const uint4* src = reinterpret_cast<const uint4*>(a.tabs + (size_t)prime * TAB_BYTES);
     uint4* dst = reinterpret_cast<uint4*>(sm + S.ba);  // BA | BB0 | BB1 | TW are contiguous
     for (int k = tid; k < TAB_BYTES / 16; k += NTHREADS) dst[k] = src[k];
-    for (int k = tid; k < L * 32; k += NTHREADS) {  // row 2*SA = 84: ones; rows 85..95 zero
-      const int i = k >> 5, w = k & 31;
-      uint32_t* t = reinterpret_cast<uint32_t*>(sm + S.aa + i * AA_BYTES);
-      t[(2 * SA) * 32 + w] = 0x01010101u;
-      for (int r = 2 * SA + 1; r < KA; ++r) t[r * 32 + w] = 0u;
-    }
   }
   if (tid == 0) {
-    // arrivals per phase: producer / epilogue warps, or one tcgen05.commit / expect_tx
+    // arrivals per phase: epilogue warps, or one tcgen05.commit / expect_tx
     for (int i = 0; i < NBARS; ++i)
-      mbar_init(bar(i), (i == AA_FULL || i == XA_EMPTY0 || i == XA_EMPTY1) ? (uint32_t)NPROD
-                        : (i == TA_EMPTY || i == AB_FULL0 || i == AB_FULL1) ? (uint32_t)EA_WARPS
+      mbar_init(bar(i), (i == TA_EMPTY || i == AB_FULL0 || i == AB_FULL1) ? (uint32_t)EA_WARPS
                         : (i == TB_EMPTY0 || i == TB_EMPTY1) ? (uint32_t)(EB_WARPS / 2) : 1u);  // per k1-half
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -156,91 +146,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  if (warp >= PROD_WARP0 && warp < MMA_WARP) {
-    // ------------------------------ producers ------------------------------
-    const int ptid = tid - PROD_WARP0 * 32;
-    uint32_t gr = 0, pi = 0;
-    const uint32_t magic = rc.magicM;
-    const uint32_t xa_s = su32(sm + S.xa);
+  if (warp == LOAD_WARP) {
+    // ------------------------------ loader: pass-A operand tiles of each rep (digits kernel) ------------------------------
+    // the L digit tiles of (row pair, rep) are contiguous in the workspace: one bulk copy per rep
+    // into the rep's buffer (two buffers, so the next rep streams in while this one is multiplied)
+    uint32_t gr = 0;
     int tn = 0;
-    // one bulk copy per row, each on its own barrier: row s of the next pair is fetched as soon
-    // as every producer is past row s of this pair's last rep (the other row is still in use)
-    auto load_row = [&](int64_t rp_, int s_) {
-      const int64_t row = 2 * rp_ + s_;
-      if (row < a.B) {
-        mbar_expect_tx(bar(XA_FULL0 + s_), (uint32_t)(N * 8));
-        bulk_copy(xa_s + s_ * N * 8, a.in + row * 2 * (int64_t)N, N * 8, bar(XA_FULL0 + s_));
-      } else {
-        mbar_arrive(bar(XA_FULL0 + s_));
-      }
-    };
-    if (ptid == 0 && slot < npairs) {
-      load_row(slot, 0);
-      load_row(slot, 1);
-    }
-    for (int64_t rp = slot; rp < npairs; rp += a.cpp, ++pi) {
-      const int64_t row0 = 2 * rp;
-      const int nrows = a.B - row0 < 2 ? (int)(a.B - row0) : 2;
-      trace(a, 0, tn, ptid == 0);
-      for (int r = 0; r < a.nreps; ++r, ++gr) {
-        mbar_wait_sleep(bar(AA_EMPTY), (gr & 1) ^ 1);
-        trace(a, 0, tn, ptid == 0);
-        const uint32_t dinv = a.dinv[r];
-        const uint32_t step1 = fastmod((uint32_t)N1 * dinv, M, magic);
-#pragma unroll 1
-        for (int s = 0; s < 2; ++s) {
-          if (r == 0) mbar_wait_sleep(bar(XA_FULL0 + s), pi & 1);
-          const uint64_t* xr = xa + s * N;
-          for (int u = ptid; u < UNITS / 2; u += NPROD * 32) {
-            const int g = u % 13, rest = u / 13;
-            const int m1 = rest % 7, j = rest / 7;
-            const int lane0 = g < 7 ? 4 * g : 32 + 4 * (g - 7);
-            uint32_t ev[L][4];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              const int ln = lane0 + v;
-              const int m0 = ln < 32 ? ln : ln - 7;
-              const bool ok = (ln < 32 ? m0 < 25 : true) && s < nrows;
-              uint64_t y = 0;
-              if (ok) {
-                const uint32_t m = (uint32_t)(m1 * SB + m0);
-                const uint32_t s1 = fastmod(m * dinv, M, magic);
-                const uint32_t s1j = fastmod(s1 + (uint32_t)j * step1, M, magic);  // (j n1 + m) dinv mod M
-                const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, magic);
-                const uint64_t v1 = s1j < (uint32_t)N ? xr[s1j] : 0ull;
-                const uint64_t v2 = s2 < (uint32_t)N ? xr[s2] : 0ull;
-                y = (v1 - v2) & QMASK;
-              }
-              int dg[L];
-              decompose<L>(y, dg, rc);
-#pragma unroll
-              for (int i = 0; i < L; ++i) ev[i][v] = (uint32_t)(dg[i] + a.off);
-            }
-            const int q = j * 7 + m1, mlane = 64 * s + lane0;
-#pragma unroll
-            for (int i = 0; i < L; ++i) {
-              const uint32_t p01 = ev[i][0] | (ev[i][1] << 16), p23 = ev[i][2] | (ev[i][3] << 16);
-              const uint32_t lo = __byte_perm(p01, p23, 0x6420), hi = __byte_perm(p01, p23, 0x7531);
-              const uint32_t tile = aa + (uint32_t)(i * AA_BYTES);
-              asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(swz(tile, q, mlane)), "r"(lo) : "memory");
-              asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(swz(tile, SA + q, mlane)), "r"(hi) : "memory");
-            }
-          }
-          if (r == a.nreps - 1) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(XA_EMPTY0 + s));
-            if (ptid == 0) {
-              mbar_wait_sleep(bar(XA_EMPTY0 + s), pi & 1);
-              if (rp + a.cpp < npairs) load_row(rp + a.cpp, s);
-            }
-          }
+    if (lane == 0) {
+      for (int64_t rp = slot; rp < npairs; rp += a.cpp) {
+        for (int r = 0; r < a.nreps; ++r, ++gr) {
+          const uint32_t b = gr & 1;
+          mbar_wait_sleep(bar(AA_EMPTY0 + b), ((gr >> 1) & 1) ^ 1);
+          trace(a, 0, tn, true);
+          const uint32_t bytes = (uint32_t)(L * AA_BYTES);
+          mbar_expect_tx(bar(AA_FULL0 + b), bytes);
+          bulk_copy(aa + b * bytes, a.tiles + ((size_t)rp * a.nreps + r) * bytes, bytes, bar(AA_FULL0 + b));
         }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(AA_FULL));
-        trace(a, 0, tn, ptid == 0);
       }
     }
+    __syncwarp();
   } else if (warp == MMA_WARP) {
     // ------------------------------ MMA issuer ------------------------------
     constexpr uint32_t idescA = (2u << 4) | (1u << 15) | ((uint32_t)(NA >> 3) << 17) | ((128u >> 4) << 24);
@@ -272,21 +196,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int64_t rp = slot; rp < npairs; rp += a.cpp) {
       for (int r = 0; r < a.nreps; ++r, ++gr) {
         for (int i = 0; i < L; ++i, ++g) {
+          const uint32_t ab_set = gr & 1;  // pass-A operand buffer of this rep
           if (i == 0) {
-            if (g > 0) issueB(g - 1);  // before waiting on the producers' next rep
-            mbar_wait_sleep(bar(AA_FULL), gr & 1);
+            if (g > 0) issueB(g - 1);  // before waiting on the next rep's operand tiles
+            mbar_wait_sleep(bar(AA_FULL0 + ab_set), (gr >> 1) & 1);
           }
           mbar_wait_sleep(bar(TA_EMPTY), (g & 1) ^ 1);
           tc_fence_after();
           if (lane == 0) {
 #pragma unroll
             for (int j = 0; j < KA / 32; ++j) {
-              const uint64_t ad = sdesc(aa + i * AA_BYTES + j * 4096, 16, 1024, 2);
+              const uint64_t ad = sdesc(aa + (ab_set * L + i) * AA_BYTES + j * 4096, 16, 1024, 2);
               const uint64_t bd = sdesc(ba + 2 * j * kbA, kbA, 128, 0);
               mma_i8(tmem + COL_A, ad, bd, idescA, j > 0 ? 1u : 0u);
             }
             mma_commit(bar(TA_FULL));
-            if (i == L - 1) mma_commit(bar(AA_EMPTY));
+            if (i == L - 1) mma_commit(bar(AA_EMPTY0 + ab_set));
           }
           __syncwarp();
           trace(a, 1, tn, lane == 0);
@@ -295,9 +220,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
     if (g > 0) issueB(g - 1);
-  } else if (warp >= EB_WARPS && warp < PROD_WARP0) {
+  } else if (warp >= EB_WARPS && warp < LOAD_WARP) {
     // ------------------------------ E_A: pass A -> twiddle -> pass-B operand ------------------------------
-    const int q = warp & 3;
+    const int q = warp & 3, h = (warp - EB_WARPS) >> 2;
     const int s = q >> 1;
     const int m0 = (q & 1) ? 25 + lane : lane;
     const bool valid = (q & 1) ? lane < 24 : lane < 25;
@@ -314,15 +239,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           trace(a, 2, tn, tid == EB_WARPS * 32);
           mbar_wait_sleep(bar(AB_EMPTY0 + buf), ((g >> 1) & 1) ^ 1);
           const uint32_t dst = ab + buf * AB_BYTES;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {  // outputs o = 21 h + [0, 21) -> pass-B lanes 64 s + 32 h + [0, 21)
+          {  // outputs o = 21 h + [0, 21) -> pass-B lanes 64 s + 32 h + [0, 21)
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               uint32_t w[4][8];
 #pragma unroll
               for (int pl = 0; pl < 4; ++pl) tmem_ld8(trow + (uint32_t)(pl * NAO + 21 * h + 8 * c), w[pl]);
               tmem_wait_ld();
-              if (h == 1 && c == 2) {
+              if (c == 2) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(bar(TA_EMPTY));
@@ -450,6 +374,86 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512) : "memory");
 }
 
+// Digits kernel: the pass-A operand tiles of every (row pair, rep, digit), already in the UMMA
+// MN-major 128B-swizzled layout (K row kk, lane m at kk * 128 + ((m / 16) ^ (kk % 8)) * 16 + m % 16).
+// K rows: plane 0 / 1 (low / high byte of digit + offset) of input q = j * 7 + m1 at q / 42 + q,
+// row 84 all ones (offset correction), rows 85..95 zero.  Lane 64 s + (m0 < 25 ? m0 : m0 + 7) holds
+// coefficient j * 343 + m1 * 49 + m0 of row s of the pair (other lanes zero).  One CTA per row
+// pair, all reps: the automorphism gather (reference ring.py:101-130) reads the two staged rows,
+// digits are the reference's balanced decomposition (crypto.py:288-323).
+template <int L>
+__global__ void __launch_bounds__(DIG_THREADS)
+    digits_kernel(const __grid_constant__ RingConst rc, const __grid_constant__ TcFwdArgs a) {
+  __shared__ __align__(16) uint64_t xs[2 * N];
+  const int64_t rp = blockIdx.x;
+  const int64_t row0 = 2 * rp;
+  const int nrows = a.B - row0 < 2 ? (int)(a.B - row0) : 2;
+  for (int s = 0; s < 2; ++s) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.in + (row0 + s) * 2 * (int64_t)N);
+    uint4* dst = reinterpret_cast<uint4*>(xs + s * N);
+    for (int k = threadIdx.x; k < N / 2; k += DIG_THREADS)
+      dst[k] = s < nrows ? src[k] : make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const uint32_t magic = rc.magicM;
+  for (int r = 0; r < a.nreps; ++r) {
+    const uint32_t dinv = a.dinv[r];
+    unsigned char* tiles = a.tiles + ((size_t)rp * a.nreps + r) * L * AA_BYTES;
+    // constant rows 84..95 of each digit tile
+    for (int k = threadIdx.x; k < L * 12 * 8; k += DIG_THREADS) {
+      const int i = k / 96, rr = 84 + (k % 96) / 8, c = k % 8;
+      const uint32_t v = rr == 84 ? 0x01010101u : 0u;
+      *reinterpret_cast<uint4*>(tiles + i * AA_BYTES + rr * 128 + c * 16) = make_uint4(v, v, v, v);
+    }
+    // work item (q, chunk c): 16 lanes of K rows q (plane 0) and 42 + q (plane 1) in every digit tile
+    for (int it = threadIdx.x; it < SA * 8; it += DIG_THREADS) {
+      const int q = it >> 3, c = it & 7;
+      const int s = c >> 2, cc = c & 3;
+      const int j = q / 7, m1 = q - 7 * j;
+      uint32_t lo[L][4], hi[L][4];
+#pragma unroll
+      for (int i = 0; i < L; ++i)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) lo[i][w] = hi[i][w] = 0u;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int ln = 16 * cc + u;
+        const int m0 = ln < 32 ? ln : ln - 7;
+        const bool lane_ok = ln < 32 ? m0 < 25 : ln < 56;
+        if (!lane_ok) continue;
+        uint64_t y = 0;
+        if (s < nrows) {
+          const uint32_t m = (uint32_t)(m1 * SB + m0);
+          const uint32_t s1 = fastmod((uint32_t)(j * N1 + (int)m) * dinv, M, magic);
+          const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, magic);
+          const uint64_t* xr = xs + s * N;
+          const uint64_t v1 = s1 < (uint32_t)N ? xr[s1] : 0ull;
+          const uint64_t v2 = s2 < (uint32_t)N ? xr[s2] : 0ull;
+          y = (v1 - v2) & QMASK;
+        }
+        int dg[L];
+        decompose<L>(y, dg, rc);
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          const uint32_t ev = (uint32_t)(dg[i] + a.off);
+          lo[i][u >> 2] |= (ev & 255u) << (8 * (u & 3));
+          hi[i][u >> 2] |= (ev >> 8) << (8 * (u & 3));
+        }
+      }
+      const int chunk = 4 * s + cc;  // 16-byte chunk of the 128-lane K row
+#pragma unroll
+      for (int i = 0; i < L; ++i) {
+        unsigned char* t = tiles + i * AA_BYTES;
+        *reinterpret_cast<uint4*>(t + q * 128 + ((chunk ^ (q & 7)) << 4)) =
+            make_uint4(lo[i][0], lo[i][1], lo[i][2], lo[i][3]);
+        const int kh = SA + q;
+        *reinterpret_cast<uint4*>(t + kh * 128 + ((chunk ^ (kh & 7)) << 4)) =
+            make_uint4(hi[i][0], hi[i][1], hi[i][2], hi[i][3]);
+      }
+    }
+  }
+}
+
 // key spectra (CUDA-core kernel layout, K^ R mod p) -> per (slot, digit, prime) [k1][o] uint2
 // (Ka R, Kb R) = K^ R^2 mod p in the tensor-core output order (E_B: REDC(REDC(value) * K R^2) = value * K^)
 __global__ void keys_kernel(const __grid_constant__ RingConst rc, const uint32_t* spectra, int nslots,
@@ -568,8 +572,21 @@ void tc_build_tables(const RingConst& rc, const uint32_t* twid, int twid_stride_
 
 size_t tc_fwd_smem_bytes(int L) { return (size_t)tc7::Smem::make(L).total; }
 
+size_t tc_tile_bytes(const RingConst& rc, int64_t rows, int nreps) {
+  return (size_t)((rows + 1) / 2) * nreps * rc.l * tc7::AA_BYTES;
+}
+
 cudaError_t launch_tc_fwd(const RingConst& rc, const TcFwdArgs& a, cudaStream_t st) {
   if (a.B <= 0 || a.nreps <= 0) return cudaSuccess;
+  {
+    const unsigned pairs = (unsigned)((a.B + 1) / 2);
+    if (rc.l == 3)
+      tc7::digits_kernel<3><<<pairs, tc7::DIG_THREADS, 0, st>>>(rc, a);
+    else
+      tc7::digits_kernel<2><<<pairs, tc7::DIG_THREADS, 0, st>>>(rc, a);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   const size_t smem = tc_fwd_smem_bytes(rc.l);
   const int64_t npairs = (a.B + 1) / 2;
   TcFwdArgs b = a;

@@ -40,7 +40,10 @@ namespace sfhr {
 namespace ntt {
 
 constexpr int CHUNK_MAX = 8192;  // residues per CTA
-constexpr int EPT = 16;          // residues per thread in a local pass
+#ifndef NTT_EPT
+#define NTT_EPT 16
+#endif
+constexpr int EPT = NTT_EPT;     // residues per thread in a local pass
 #ifndef NTT_MINB
 #define NTT_MINB 2
 #endif

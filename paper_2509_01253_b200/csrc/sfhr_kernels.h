@@ -43,6 +43,7 @@ struct TcFwdArgs {
   const uint8_t* tabs;          // per prime constant operands (tc_table_bytes)
   const int32_t* old_idx;       // [42][49] position of (o, k1) in the CUDA-core kernel's NTT order
   uint32_t* acc;                // (B, np, 2, N) NTT-domain accumulators out
+  unsigned char* tiles;         // workspace: pass-A operand tiles [pair][rep][l] (tc_tile_bytes)
   int off;                      // digit offset (tc_digit_offset)
   int cpp;                      // CTAs per prime (set by the launcher)
   long long* trace;             // debug (SFHR_TC_TRACE): CTA 0's role event clocks, [4 roles][TC_TRACE_N]
@@ -54,6 +55,7 @@ int tc_digit_offset(const RingConst& rc);
 void tc_build_tables(const RingConst& rc, const uint32_t* twid, int twid_stride_words, uint8_t* tabs,
                      int32_t* old_idx);
 size_t tc_fwd_smem_bytes(int L);
+size_t tc_tile_bytes(const RingConst& rc, int64_t rows, int nreps);
 size_t tc_keys_bytes(const RingConst& rc, int nslots);
 cudaError_t launch_tc_fwd(const RingConst& rc, const TcFwdArgs& a, cudaStream_t st);
 cudaError_t launch_tc_keys(const RingConst& rc, const uint32_t* spectra, int nslots, const int32_t* old_idx,
