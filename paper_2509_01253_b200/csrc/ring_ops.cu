@@ -309,6 +309,158 @@ __global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(con
   }
 }
 
+// Many-power variant (gamma = 2: 42 powers at b = 12, 20 at b = 16).  The row terms of every
+// power are summed in registers: one CTA per (chunk, component, tile of EXM_ROWS rows inside one
+// run of n1 rows, where c_i = i / n1 + 1 is constant).  Powers stream through shared memory: the
+// raw component arrives by bulk copy two powers ahead and is turned into the same M^-1-scaled
+// difference array as extract_ext_kernel (double-buffered: power q + 1 is staged while q is
+// accumulated); every output lane is written once.
+#ifndef SFHR_EXM_ROWS
+#define SFHR_EXM_ROWS 8
+#endif
+constexpr int EXM_ROWS = SFHR_EXM_ROWS;
+template <int T> struct ExmGeo {  // production rows: t = 7 (alpha 4), 5 (alpha 5), 3 (alpha 7)
+  static constexpr int N1 = T == 7 ? 343 : T == 5 ? 625 : 729;
+  static constexpr int THREADS = (N1 + 31) / 32 * 32;
+};
+
+// Thread f < n1 owns the t-1 lanes k = f + n1 m of its component; they share the folded position
+// N + (k mod n1) = N + f, so per (row, power) the folded term D[i d + N + f] is loaded once and
+// summed separately (subtracted at the end): 1 + 1 / (t - 1) shared loads and one 64-bit add per
+// output lane and power.
+template <int T>
+__global__ void __launch_bounds__(ExmGeo<T>::THREADS, 1) extract_many_kernel(const __grid_constant__ RingConst rc,
+                                                                            const __grid_constant__ ExtractArgs a) {
+  constexpr int N1 = ExmGeo<T>::N1, THREADS = ExmGeo<T>::THREADS, LPT = T - 1;
+  // shared: [2][M + N] difference arrays, [2][M] raw power components (zero beyond N), 2 mbarriers
+  extern __shared__ __align__(16) uint64_t sd[];
+  __shared__ uint2 soff[2][EXM_ROWS];  // per staged power: offsets i d, i d + N (mod M)
+  __shared__ __align__(8) uint64_t sbar[2];
+  const int N = rc.N, M = rc.M, L = M + N;
+  const int RS = (M + 1) & ~1;  // raw buffer stride (16-byte aligned bulk-copy destinations)
+  uint64_t* raw = sd + 2 * ((L + 1) & ~1);
+  constexpr int tiles_per_run = (N1 + EXM_ROWS - 1) / EXM_ROWS;
+  int64_t b = blockIdx.x;
+  const int tile = (int)(b % tiles_per_run);
+  b /= tiles_per_run;
+  const int run = (int)(b % (T - 1));
+  b /= T - 1;
+  const int comp = (int)(b & 1);
+  const int j = (int)(b >> 1);
+  const int i0 = run * N1 + tile * EXM_ROWS;
+  const int i1 = min(run * N1 + N1, i0 + EXM_ROWS);
+  const int64_t g0 = (int64_t)j * N + i0;
+  if (g0 >= a.E) return;
+  const int nrows = (int)min((int64_t)(i1 - i0), a.E - g0);
+  const int c = a.cvec[i0];  // constant over the run
+  const uint64_t cu = a.cu;
+  const uint64_t* src = a.power + (int64_t)j * a.npow * 2 * N + (int64_t)comp * N;  // power q at + q 2N
+  const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&sbar[0]);
+  const int f = threadIdx.x;
+  const bool act = f < N1;
+
+  // raw components arrive by bulk copy (TMA engine, no registers), two powers ahead
+  auto fetch = [&](int q) {
+    const uint32_t bar = bar0 + 8u * (q & 1);
+    const uint32_t bytes = (uint32_t)N * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(raw + (q & 1) * RS)),
+                 "l"(src + (int64_t)q * 2 * N), "r"(bytes), "r"(bar)
+                 : "memory");
+  };
+  auto wait_raw = [&](int q) {
+    const uint32_t bar = bar0 + 8u * (q & 1), parity = (uint32_t)((q >> 1) & 1);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                   " selp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done)
+                   : "r"(bar), "r"(parity)
+                   : "memory");
+  };
+  // difference array of power q from its raw component: D[x] = cu (ct[x mod M] - ct[(x - s) mod M])
+  auto stage = [&](int q, int buf) {
+    const uint32_t d = a.exps[q];
+    const uint32_t sh = fastmod((uint32_t)(c * N1) * d, M, rc.magicM);
+    const uint64_t* rw = raw + (q & 1) * RS;
+    uint64_t* D = sd + buf * L;
+    for (int x = threadIdx.x; x < L; x += THREADS) {
+      const uint32_t xm = x >= M ? x - M : x;
+      const uint32_t y = xm >= sh ? xm - sh : xm + M - sh;
+      D[x] = (rw[xm] - rw[y]) * cu;
+    }
+    if (threadIdx.x < EXM_ROWS) {
+      const uint32_t id = fastmod((uint32_t)(i0 + threadIdx.x) * d, M, rc.magicM);
+      soff[buf][threadIdx.x] = make_uint2(id, id + (uint32_t)N >= (uint32_t)M ? id + N - M : id + N);
+    }
+  };
+
+  for (int x = N + threadIdx.x; x < M; x += THREADS) raw[x] = raw[RS + x] = 0ull;  // zero tails
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0 + 8u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fetch(0);
+    if (a.npow > 1) fetch(1);
+  }
+
+  uint64_t acc[EXM_ROWS][LPT], accf[EXM_ROWS];
+#pragma unroll
+  for (int r = 0; r < EXM_ROWS; ++r) {
+    accf[r] = 0;
+#pragma unroll
+    for (int l = 0; l < LPT; ++l) acc[r][l] = 0;
+  }
+
+  wait_raw(0);
+  stage(0, 0);
+  __syncthreads();
+  if (threadIdx.x == 0 && a.npow > 2) fetch(2);  // raw buffer 0 is free again
+  for (int q = 0; q < a.npow; ++q) {
+    if (q + 1 < a.npow) {  // overlaps the accumulation below
+      wait_raw(q + 1);
+      stage(q + 1, (q + 1) & 1);
+    }
+    if (act) {
+      const char* Db = reinterpret_cast<const char*>(sd + (q & 1) * L);
+#pragma unroll
+      for (int r = 0; r < EXM_ROWS; ++r) {
+        const uint2 o = soff[q & 1][r];
+        const char* p0 = Db + 8u * (o.x + f);
+        accf[r] += *reinterpret_cast<const uint64_t*>(Db + 8u * (o.y + f));
+#pragma unroll
+        for (int l = 0; l < LPT; ++l) acc[r][l] += *reinterpret_cast<const uint64_t*>(p0 + 8 * l * N1);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && q + 3 < a.npow) fetch(q + 3);  // raw buffer (q + 1) & 1 is free
+  }
+  if (act) {
+    uint64_t* dst = a.rows + g0 * 2 * N + (int64_t)comp * N + f;
+#pragma unroll
+    for (int r = 0; r < EXM_ROWS; ++r)
+      if (r < nrows)
+#pragma unroll
+        for (int l = 0; l < LPT; ++l) dst[(int64_t)r * 2 * N + l * N1] = (acc[r][l] - accf[r]) & QMASK;
+  }
+}
+
+template <int T>
+static cudaError_t launch_many(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)(2 * ((rc.M + rc.N + 1) & ~1) + 2 * ((rc.M + 1) & ~1)) * 8;
+  cudaError_t e = cudaFuncSetAttribute(extract_many_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = (int64_t)((ExmGeo<T>::N1 + EXM_ROWS - 1) / EXM_ROWS) * (T - 1);
+  const int64_t grid = (int64_t)a.k_chunks * 2 * tiles;
+  extract_many_kernel<T><<<(unsigned)grid, ExmGeo<T>::THREADS, smem, st>>>(rc, a);
+  return cudaGetLastError();
+}
+
 template <int NP>
 static cudaError_t launch_ext(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
   const size_t both = (size_t)2 * NP * (rc.M + rc.N) * 8;
@@ -337,6 +489,11 @@ cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream
       case 5: return launch_ext<5>(rc, a, st);
       default: return launch_ext<6>(rc, a, st);
     }
+  }
+  if (a.npow > EXX_MAXPOW && !getenv("SFHR_EXTRACT_TILED") && (size_t)(2 * (rc.M + rc.N) + 2 * rc.M) * 8 <= 200 * 1024) {
+    if (rc.t == 7 && rc.alpha == 4) return launch_many<7>(rc, a, st);
+    if (rc.t == 5 && rc.alpha == 5) return launch_many<5>(rc, a, st);
+    if (rc.t == 3 && rc.alpha == 7) return launch_many<3>(rc, a, st);
   }
   const size_t smem = extract_tiled_smem(rc, a.npow);
   if (a.npow <= EX_MAXPOW && smem <= 200 * 1024) {
