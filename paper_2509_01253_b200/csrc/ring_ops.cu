@@ -449,9 +449,13 @@ __global__ void __launch_bounds__(ExmGeo<T>::THREADS, 1) extract_many_kernel(con
   }
 }
 
+static size_t exm_smem(const RingConst& rc) {  // [2][M + N] difference arrays + [2][M] raw components
+  return (size_t)(2 * ((rc.M + rc.N + 1) & ~1) + 2 * ((rc.M + 1) & ~1)) * 8;
+}
+
 template <int T>
 static cudaError_t launch_many(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
-  const size_t smem = (size_t)(2 * ((rc.M + rc.N + 1) & ~1) + 2 * ((rc.M + 1) & ~1)) * 8;
+  const size_t smem = exm_smem(rc);
   cudaError_t e = cudaFuncSetAttribute(extract_many_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -476,8 +480,24 @@ static cudaError_t launch_ext(const RingConst& rc, const ExtractArgs& a, cudaStr
   return cudaGetLastError();
 }
 
+// powers from which the many-power kernel takes over (SFHR_EXM_MIN_POW for A/B).  A/B on B200:
+// ResNet-20 b = 12 gamma = 1 (6 powers) extraction 7.90 -> 6.22 ms per inference; b = 16 gamma = 1
+// (4 powers) unchanged (ResNet-18 73.9 vs 73.7 ms), so the offset-table kernel keeps < 6 powers
+static int exm_min_pow() {
+  static const int v = [] {
+    const char* e = getenv("SFHR_EXM_MIN_POW");
+    return e ? atoi(e) : 6;
+  }();
+  return v;
+}
+
 cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
   if (a.E == 0) return cudaSuccess;
+  if (a.npow >= exm_min_pow() && !getenv("SFHR_EXTRACT_TILED") && exm_smem(rc) <= 200 * 1024) {
+    if (rc.t == 7 && rc.alpha == 4) return launch_many<7>(rc, a, st);
+    if (rc.t == 5 && rc.alpha == 5) return launch_many<5>(rc, a, st);
+    if (rc.t == 3 && rc.alpha == 7) return launch_many<3>(rc, a, st);
+  }
   // SFHR_EXTRACT_TILED=1 forces the general kernels (the tests compare both paths)
   if (a.npow >= 1 && a.npow <= EXX_MAXPOW && (size_t)a.npow * (rc.M + rc.N) * 8 <= EXX_SMEM_MAX &&
       !getenv("SFHR_EXTRACT_TILED")) {
@@ -489,11 +509,6 @@ cudaError_t launch_extract(const RingConst& rc, const ExtractArgs& a, cudaStream
       case 5: return launch_ext<5>(rc, a, st);
       default: return launch_ext<6>(rc, a, st);
     }
-  }
-  if (a.npow > EXX_MAXPOW && !getenv("SFHR_EXTRACT_TILED") && (size_t)(2 * (rc.M + rc.N) + 2 * rc.M) * 8 <= 200 * 1024) {
-    if (rc.t == 7 && rc.alpha == 4) return launch_many<7>(rc, a, st);
-    if (rc.t == 5 && rc.alpha == 5) return launch_many<5>(rc, a, st);
-    if (rc.t == 3 && rc.alpha == 7) return launch_many<3>(rc, a, st);
   }
   const size_t smem = extract_tiled_smem(rc, a.npow);
   if (a.npow <= EX_MAXPOW && smem <= 200 * 1024) {

@@ -79,10 +79,10 @@ def test_extract_one_and_full_chunk(b):
         partial_extract(bundle, None, R.N + 1, Rm)
 
 
-@pytest.mark.parametrize("b,gamma", [(8, 0), (12, 0), (16, 0), (8, 1), (12, 1), (16, 1), (12, 2), (16, 2)])
+@pytest.mark.parametrize("b,gamma", [(8, 0), (12, 0), (16, 0), (8, 1), (12, 1), (16, 1), (8, 2), (12, 2), (16, 2)])
 def test_extract_kernels_agree(b, gamma, monkeypatch):
-    """The offset-table kernel (<= 6 powers; one component at a time when both do not fit), the
-    general kernels and the oracle agree bit for bit."""
+    """The offset-table kernel (< 6 powers; one component at a time when both do not fit), the
+    many-power kernel (>= 6 powers), the general kernels and the oracle agree bit for bit."""
     from paper_2509_01253_b200.params import RingParams
     from paper_2509_01253_b200.tracepack import PowerBundle, partial_extract, power_exponents
     from paper_2509_01253_b200.keyswitch import RlweCiphertext
