@@ -203,8 +203,9 @@ size_t extract_tiled_smem(const RingConst& rc, int npow) { return (size_t)npow *
 // is constant over long runs of rows, so per distinct c of the CTA's row tile each power is
 // staged once as the DIFFERENCE array D[x] = cu (ct[x mod M] - ct[(x - s) mod M]) (ct = 0 at
 // indices >= N), extended to length M + N so that both reads are D[o + k] / D[o' + k mod n1]
-// with per-(row, power) offsets o = i d, o' = i d + N precomputed once: 2 shared loads and 2
-// adds per (output, power), no modular index arithmetic per element.  When both components of
+// with per-(row, power) offsets o = i d, o' = i d + N precomputed once, no modular index
+// arithmetic per element.  A thread owns the t - 1 lanes f + n1 m of a component, which share
+// the folded read D[o' + f]: 1 + 1 / (t - 1) shared loads per (output, power).  When both components of
 // all powers do not fit in shared memory (SPLIT) the CTA stages one component at a time.
 // M^-1 (cu) is folded into the staged values: (sum +-ct) cu = sum +-(ct cu) mod 2^64.
 constexpr int EXX_MAXPOW = 6;
@@ -223,7 +224,7 @@ template <bool SPLIT> struct ExxGeo {
   static constexpr int ROWS = SPLIT ? SFHR_EXX_SPLIT_MULT * EXX_ROWS : EXX_ROWS;
 };
 
-template <int NP, bool SPLIT>
+template <int NP, bool SPLIT, int LPT>
 __global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(const __grid_constant__ RingConst rc,
                                                                              const __grid_constant__ ExtractArgs a) {
   constexpr int EXX_ROWS = ExxGeo<SPLIT>::ROWS, EX_THREADS = ExxGeo<SPLIT>::THREADS;
@@ -279,28 +280,33 @@ __global__ void __launch_bounds__(ExxGeo<SPLIT>::THREADS) extract_ext_kernel(con
         se[idx] = v * cu;
       }
       __syncthreads();
-      const int lane0 = SPLIT ? part * N : 0, lane1 = SPLIT ? lane0 + N : 2 * N;
-      for (int lane = lane0 + threadIdx.x; lane < lane1; lane += EX_THREADS) {
-        const int comp = lane >= N;
-        const int k = lane - comp * N;
-        const int kf = (int)fastmod((uint32_t)k, n1, rc.magicN1);
-        const char* ek = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + k);
-        const char* ef = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + kf);
-        uint64_t* dst = a.rows + g0 * 2 * N + lane;
+      // work item = (component, fold position f < n1): the t-1 lanes k = f + n1 m of a row share
+      // the folded read D[i d + N + f], loaded once per (row, power)
+      const int w1 = (SPLIT ? 1 : 2) * n1;
+      for (int w = threadIdx.x; w < w1; w += EX_THREADS) {
+        const int comp = SPLIT ? part : (w >= n1);
+        const int f = w - (SPLIT ? 0 : comp) * n1;
+        const char* ek = sb + 8 * ((SPLIT ? 0 : comp * NP * L) + f);
+        uint64_t* dst = a.rows + g0 * 2 * N + (int64_t)comp * N + f;
         auto row = [&](int r) {
-          uint64_t acc = 0;
+          uint64_t fold = 0, acc[LPT];
+#pragma unroll
+          for (int m = 0; m < LPT; ++m) acc[m] = 0;
 #pragma unroll
           for (int q = 0; q < NP; ++q) {
             const uint2 o = soff[r][q];
-            acc += *reinterpret_cast<const uint64_t*>(ek + o.x) - *reinterpret_cast<const uint64_t*>(ef + o.y);
+            fold += *reinterpret_cast<const uint64_t*>(ek + o.y);
+#pragma unroll
+            for (int m = 0; m < LPT; ++m) acc[m] += *reinterpret_cast<const uint64_t*>(ek + o.x + 8 * m * n1);
           }
-          dst[(int64_t)r * 2 * N] = acc & QMASK;
+#pragma unroll
+          for (int m = 0; m < LPT; ++m) dst[(int64_t)r * 2 * N + m * n1] = (acc[m] - fold) & QMASK;
         };
         if (ncv == 1) {  // the common case: one c_i for the whole tile, no per-row test
-#pragma unroll 4
+#pragma unroll 2
           for (int r = 0; r < nrows; ++r) row(r);
         } else {
-#pragma unroll 4
+#pragma unroll 2
           for (int r = 0; r < nrows; ++r)
             if (srow_c[r] == c) row(r);
         }
@@ -465,12 +471,12 @@ static cudaError_t launch_many(const RingConst& rc, const ExtractArgs& a, cudaSt
   return cudaGetLastError();
 }
 
-template <int NP>
-static cudaError_t launch_ext(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
+template <int NP, int LPT>
+static cudaError_t launch_ext_t(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
   const size_t both = (size_t)2 * NP * (rc.M + rc.N) * 8;
   const bool split = both > EXX_SMEM_MAX;
   const size_t smem = split ? both / 2 : both;
-  const auto kern = split ? extract_ext_kernel<NP, true> : extract_ext_kernel<NP, false>;
+  const auto kern = split ? extract_ext_kernel<NP, true, LPT> : extract_ext_kernel<NP, false, LPT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int rows = split ? ExxGeo<true>::ROWS : ExxGeo<false>::ROWS;
@@ -478,6 +484,16 @@ static cudaError_t launch_ext(const RingConst& rc, const ExtractArgs& a, cudaStr
   const int rblocks = (rc.N + rows - 1) / rows;
   kern<<<(unsigned)(a.k_chunks * rblocks), threads, smem, st>>>(rc, a);
   return cudaGetLastError();
+}
+
+template <int NP>
+static cudaError_t launch_ext(const RingConst& rc, const ExtractArgs& a, cudaStream_t st) {
+  switch (rc.t) {  // lanes per fold position: t - 1
+    case 3: return launch_ext_t<NP, 2>(rc, a, st);
+    case 5: return launch_ext_t<NP, 4>(rc, a, st);
+    case 7: return launch_ext_t<NP, 6>(rc, a, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // powers from which the many-power kernel takes over (SFHR_EXM_MIN_POW for A/B).  A/B on B200:
