@@ -55,7 +55,8 @@ struct sfhr_key {
   std::map<uint32_t, int> slot;  // d -> slot
   uint32_t* spectra = nullptr;   // [nidx][l][2][np][N]
   size_t slot_words = 0;
-  uint2* tc_keys = nullptr;      // [nidx][l][np][49][42] tensor-core MAC operands (tc path only)
+  mutable uint2* tc_keys = nullptr;  // [nidx][l][np][49][42] tensor-core MAC operands, built on first use
+  int nidx = 0;
 };
 
 namespace {
@@ -185,7 +186,13 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     if (in != out) CK(cudaMemcpyAsync(out, in, (size_t)B * 2 * P.rc.N * 8, cudaMemcpyDeviceToDevice, st), "stage copy");
     return SFHR_OK;
   }
-  if (ctx->tc_min_reps > 0 && ctx->tc_tabs && key->tc_keys && ns >= ctx->tc_min_reps) {
+  const bool use_tc = ctx->tc_min_reps > 0 && ctx->tc_tabs && key->nidx > 0 && ns >= ctx->tc_min_reps;
+  if (use_tc && !key->tc_keys) {  // the tensor-core MAC operands of this key set, on first use
+    CK(cudaMalloc(reinterpret_cast<void**>(&key->tc_keys), tc_keys_bytes(P.rc, key->nidx)), "tc key alloc");
+    CK(launch_tc_keys(P.rc, key->spectra, key->nidx, ctx->tc_oldidx, key->tc_keys, st), "tc key kernel");
+    ++g_launches;
+  }
+  if (use_tc) {
     // tensor-core forward (NTT-domain accumulators) + the CUDA-core kernel's inverse / CRT tail,
     // in chunks whose accumulators (49 KB per row at b = 12) stay L2-sized
     TcFwdArgs f;
@@ -476,14 +483,9 @@ int sfhr_register_ksk(sfhr_ctx* ctx, const uint32_t* idx, int nidx, const uint64
   a.twid = ctx->twid;
   e = launch_spectra(rc, a, nidx * rc.l * 2, (cudaStream_t)stream);
   if (nidx) ++g_launches;
-  if (e == cudaSuccess && ctx->tc_tabs && nidx > 0) {
-    e = cudaMalloc(&key->tc_keys, tc_keys_bytes(rc, nidx));
-    if (e == cudaSuccess) e = launch_tc_keys(rc, key->spectra, nidx, ctx->tc_oldidx, key->tc_keys, (cudaStream_t)stream);
-    if (e == cudaSuccess) ++g_launches;
-  }
+  key->nidx = nidx;
   if (e != cudaSuccess) {
     cudaFree(key->spectra);
-    cudaFree(key->tc_keys);
     delete key;
     return cuda_fail(e, "ksk spectra kernel");
   }
