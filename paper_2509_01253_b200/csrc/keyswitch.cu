@@ -495,6 +495,25 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
     uint64_t bsum = a.identity ? xin[N + k] : 0ull;
     const uint32_t kmod = (uint32_t)(k % n1);
+#if SFHR_BODY_UNROLL
+    // every rep's two gathers in flight before the first add (the loop was latency-serialised)
+    uint64_t g1[SFHR_BODY_UNROLL], g2[SFHR_BODY_UNROLL];
+    for (int r0 = 0; r0 < a.nreps; r0 += SFHR_BODY_UNROLL) {
+#pragma unroll
+      for (int u = 0; u < SFHR_BODY_UNROLL; ++u) {
+        g1[u] = g2[u] = 0ull;
+        if (r0 + u < a.nreps) {
+          const uint32_t dinv = a.dinv[r0 + u];
+          const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
+          const uint32_t s2 = fastmod((uint32_t)(N + kmod) * dinv, M, rc.magicM);
+          if (s1 < (uint32_t)N) g1[u] = xin[N + s1];
+          if (s2 < (uint32_t)N) g2[u] = xin[N + s2];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < SFHR_BODY_UNROLL; ++u) bsum += g1[u] - g2[u];
+    }
+#else
     for (int r = 0; r < a.nreps; ++r) {
       const uint32_t dinv = a.dinv[r];
       const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
@@ -503,6 +522,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       if (s2 < (uint32_t)N) v -= xin[N + s2];
       bsum += v;
     }
+#endif
     bsum_s[k - k0] = bsum;
   }
 
@@ -545,6 +565,9 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   }
 }
 
+#ifndef SFHR_BODY_UNROLL
+#define SFHR_BODY_UNROLL 0
+#endif
 #ifndef SFHR_ROWS_PER_CLUSTER
 #define SFHR_ROWS_PER_CLUSTER 1
 #endif

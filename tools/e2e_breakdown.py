@@ -12,13 +12,15 @@ from paper_2509_01253_b200.keyswitch import KeySwitchKeySet  # noqa: E402
 from paper_2509_01253_b200.params import preset_for_bits  # noqa: E402
 from paper_2509_01253_b200.device import to_host_u64  # noqa: E402
 
-sch = preset_for_bits(12, 0)
+import os
+GAMMA = int(os.environ.get("GAMMA", "0"))
+sch = preset_for_bits(12, GAMMA)
 model = bench.make_model("resnet20", 12, 0)
 eng = ServerEngine(model, sch, master_seed=bytes(32), device=0)
 keys = bench.synthetic_ksk(sch, 0)
 kid = eng.register_client(KeySwitchKeySet(keys, sch.gadget, 0.0, sch.ring))
 powers, exps = bench.synthetic_inputs(model, sch, 1000)
-bundles = [bench.as_bundles(p, exps, 0) for p in powers]
+bundles = [bench.as_bundles(p, exps, GAMMA) for p in powers]
 acc = {}
 
 
