@@ -166,3 +166,28 @@ def test_concurrent_sessions_match_sequential():
         t.join()
     for i in range(3):
         assert np.array_equal(seq[i], par[i]), i
+
+
+@pytest.mark.parametrize("b,gamma,E_frac", [(12, 2, 2.4), (16, 2, 1.7), (12, 1, 2.4), (8, 2, 1.3), (16, 1, 2.0)])
+def test_extract_multi_chunk_ragged(b, gamma, E_frac):
+    """Several chunks and a ragged last one through extract_device (the round path): rows of
+    chunk j are extracted from chunk j's powers only, the tail stops at E, bit-exact vs the
+    oracle chunk by chunk (many-power and offset-table kernels)."""
+    import torch
+    from paper_2509_01253_b200.params import RingParams
+    from paper_2509_01253_b200.device import RingContext, to_dev, to_host_u64
+    from paper_2509_01253_b200.tracepack import extract_device, power_exponents
+    sch = osc.preset(b, gamma)
+    R = sch.ring
+    Rm = RingParams(R.t, R.alpha, R.p_bits)
+    exps = power_exponents(gamma, Rm)
+    E = int(E_frac * R.N)
+    k = -(-E // R.N)
+    power = u53(300 + b + gamma, (k, len(exps), 2, R.N))
+    ctx = RingContext.get(R.t, R.alpha, R.p_bits, sch.gadget.D, sch.gadget.l, gamma, 0, 0)
+    rows = to_host_u64(extract_device(ctx, to_dev(power, ctx.dev), exps, E))
+    assert rows.shape == (E, 2, R.N)
+    for j in range(k):
+        cnt = min(R.N, E - j * R.N)
+        ob = opk.Bundle(gamma, {d: oks.Ct(power[j, q, 0], power[j, q, 1]) for q, d in enumerate(exps)})
+        assert np.array_equal(rows[j * R.N:j * R.N + cnt], opk.extract(ob, cnt, R)), j
