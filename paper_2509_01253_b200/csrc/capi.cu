@@ -122,6 +122,41 @@ int key_slot(const sfhr_key* key, uint32_t d) {
   return it->second;
 }
 
+// Clusters per row of a representative-split launch: enough to give ~SFHR_REP_SPLIT clusters per
+// SM when a launch has few rows (default 1; 0 disables)
+int rep_split(int nreps, int64_t B) {
+  static const int enabled = [] {
+    const char* e = std::getenv("SFHR_REP_SPLIT");
+    return e ? std::atoi(e) : 1;
+  }();
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (!enabled || nreps < 2 || B <= 0) return 1;
+  const int64_t want = (int64_t)enabled * nsm / B;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(nreps, want));
+}
+
+// grow-only device workspace of a context, shared by the tensor-core and representative-split
+// paths; a call waits (stream-ordered) for the previous user recorded on tc_ws_free
+int workspace(sfhr_ctx* ctx, size_t bytes, cudaStream_t st, uint32_t** out) {
+  if (!ctx->tc_ws_free) CK(cudaEventCreateWithFlags(&ctx->tc_ws_free, cudaEventDisableTiming), "workspace event");
+  if (bytes > ctx->tc_ws_bytes) {  // grow (rare): wait for the last user before freeing
+    CK(cudaEventSynchronize(ctx->tc_ws_free), "workspace sync");
+    cudaFree(ctx->tc_ws);
+    ctx->tc_ws = nullptr;
+    ctx->tc_ws_bytes = 0;
+    CK(cudaMalloc(reinterpret_cast<void**>(&ctx->tc_ws), bytes), "workspace alloc");
+    ctx->tc_ws_bytes = bytes;
+  }
+  CK(cudaStreamWaitEvent(st, ctx->tc_ws_free, 0), "workspace wait");  // a previous caller's stream
+  *out = ctx->tc_ws;
+  return SFHR_OK;
+}
+
 int64_t tc_chunk_rows() {
   static const int64_t rows = [] {
     const char* e = std::getenv("SFHR_TC_CHUNK");
@@ -213,17 +248,8 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     const size_t acc_bytes = (size_t)std::min<int64_t>(B, chunk) * P.rc.np * 2 * P.rc.N * 4;
     const size_t tile_bytes = tc_tile_bytes(P.rc, std::min<int64_t>(B, chunk), ns);
     const size_t ws_bytes = ((acc_bytes + 1023) & ~(size_t)1023) + tile_bytes;
-    if (!ctx->tc_ws_free) CK(cudaEventCreateWithFlags(&ctx->tc_ws_free, cudaEventDisableTiming), "tc event");
-    if (ws_bytes > ctx->tc_ws_bytes) {  // grow (rare): wait for the last user before freeing
-      CK(cudaEventSynchronize(ctx->tc_ws_free), "tc workspace sync");
-      cudaFree(ctx->tc_ws);
-      ctx->tc_ws = nullptr;
-      ctx->tc_ws_bytes = 0;
-      CK(cudaMalloc(reinterpret_cast<void**>(&ctx->tc_ws), ws_bytes), "tc workspace alloc");
-      ctx->tc_ws_bytes = ws_bytes;
-    }
-    CK(cudaStreamWaitEvent(st, ctx->tc_ws_free, 0), "tc workspace wait");  // a previous caller's stream
-    uint32_t* acc = ctx->tc_ws;
+    uint32_t* acc = nullptr;
+    if (const int rc_ = workspace(ctx, ws_bytes, st, &acc)) return rc_;
     f.tiles = reinterpret_cast<unsigned char*>(ctx->tc_ws) + ((acc_bytes + 1023) & ~(size_t)1023);
     for (int64_t r0 = 0; r0 < B; r0 += chunk) {
       const int64_t nb = std::min<int64_t>(chunk, B - r0);
@@ -266,6 +292,22 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     }
     CK(cudaEventRecord(ctx->tc_ws_free, st), "tc workspace release");
     --g_launches;  // counted once below (digits + tensor-core forward + inverse per chunk)
+  } else if (const int split = rep_split(ns, B); split > 1) {
+    // few rows (late tower stages, small models): the representatives of a row are spread over
+    // `split` clusters whose NTT-domain partial sums the second launch adds before the inverse
+    const size_t ws_bytes = (size_t)B * split * P.rc.np * 2 * P.rc.N * 4;
+    uint32_t* ws = nullptr;
+    if (const int rc_ = workspace(ctx, ws_bytes, st, &ws)) return rc_;
+    StageArgs s1 = a;
+    s1.acc_out = ws;
+    s1.nsplit = split;
+    CK(launch_stage(P.rc, s1, st), "stage kernel (representative split)");
+    StageArgs s2 = a;
+    s2.acc_in = ws;
+    s2.nsplit = split;
+    CK(launch_stage(P.rc, s2, st), "stage kernel (inverse / CRT)");
+    CK(cudaEventRecord(ctx->tc_ws_free, st), "workspace release");
+    ++g_launches;
   } else {
     CK(launch_stage(P.rc, a, st), "stage kernel");
   }

@@ -307,7 +307,7 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst
 
 template <int T, int A, int L, int PR>
 __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& a, unsigned char* smem,
-                                          const int64_t row, const bool stage_twiddles) {
+                                          const int64_t row, const bool stage_twiddles, const int split = 0) {
   const PrimeConst& pc = rc.pc[PR];
   const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
   const Geo<T, A> g(rc);
@@ -341,29 +341,47 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   }
   const int per = (N + rc.np - 1) / rc.np;
   const int k0 = PR * per, k1 = min(N, k0 + per);
+  // this cluster's representatives (all of them unless the launch splits them, acc_out); the
+  // split launch counts its own reps, so the acc_in launch that sums the partials does not
+  const int nsp = a.acc_out && a.nsplit > 1 ? a.nsplit : 1;
+  const int rb = split * a.nreps / nsp, re = (split + 1) * a.nreps / nsp;
+  const bool counts = !(a.acc_in && a.nsplit > 1);
   if (!live) {
-    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-      xout[k] = 0;
-      xout[N + k] = 0;
-    }
-    if (PR == 0 && threadIdx.x == 0 && a.counter && !a.skip_zero)
-      atomicAdd(a.counter, (unsigned long long)a.nreps);
+    if (!a.acc_out)
+      for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        xout[k] = 0;
+        xout[N + k] = 0;
+      }
+    if (PR == 0 && threadIdx.x == 0 && a.counter && !a.skip_zero && counts)
+      atomicAdd(a.counter, (unsigned long long)(re - rb));
     return;  // uniform across the cluster: every CTA saw the same row
   }
-  if (PR == 0 && threadIdx.x == 0 && a.counter) atomicAdd(a.counter, (unsigned long long)a.nreps);
+  if (PR == 0 && threadIdx.x == 0 && a.counter && counts) atomicAdd(a.counter, (unsigned long long)(re - rb));
 
   const int item = threadIdx.x;
   const bool owner = item < g.nitems;
 
   if (a.acc_in) {
-    // NTT-domain accumulators come from the tensor-core forward kernel (keyswitch_tc.cu)
-    const uint4* src = reinterpret_cast<const uint4*>(a.acc_in + ((size_t)row * rc.np + PR) * 2 * N);
+    // NTT-domain accumulators come from the tensor-core forward kernel (keyswitch_tc.cu) or
+    // from the nsplit partial sums of a representative-split launch (each < 2 p reps_s: the
+    // total stays below 2 p nreps, as in one pass)
+    const int parts = a.nsplit > 1 ? a.nsplit : 1;
     uint4* dst = reinterpret_cast<uint4*>(S.acc);
-    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) dst[c] = src[c];  // 2N u32 = N/2 uint4
+    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {  // 2N u32 = N/2 uint4
+      uint4 v = make_uint4(0, 0, 0, 0);
+      for (int q = 0; q < parts; ++q) {
+        const uint4 w = reinterpret_cast<const uint4*>(a.acc_in + (((size_t)row * parts + q) * rc.np + PR) * 2 * N)[c];
+        v.x += w.x;
+        v.y += w.y;
+        v.z += w.z;
+        v.w += w.w;
+      }
+      dst[c] = v;
+    }
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     __syncthreads();
   }
-  for (int r = 0; r < (a.acc_in ? 0 : a.nreps); ++r) {
+  for (int r = rb; r < (a.acc_in ? rb : re); ++r) {
     const uint32_t dinv = a.dinv[r];
 #if SFHR_FUSED_FIRST_STEP
     // ---- A+B fused: per column m, gather the T-1 coefficients j*n1+m of
@@ -433,7 +451,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     fwd_mid_stages<T, A, PR>(S.buf, L, rc, S.wt);
     // the staged mask is dead after the last rep's gathers: tell the peers they may push
     // their CRT residues into it (the matching wait precedes our own pushes)
-    if (r == a.nreps - 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (r == a.nreps - 1 && !a.acc_out) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     // ---- C: last stage (span 1) in registers, MAC against the key spectra ----
     if (owner) {
       const uint32_t* ks = a.spec[r];
@@ -460,12 +478,20 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       uint32_t* ab = S.acc + N + item * T;
 #pragma unroll
       for (int k = 0; k < T; ++k) {
-        const uint32_t ra = redc(ta[k], p, pinv), rb = redc(tb[k], p, pinv);
-        aa[k] = r ? aa[k] + ra : ra;
-        ab[k] = r ? ab[k] + rb : rb;
+        const uint32_t ra = redc(ta[k], p, pinv), rb2 = redc(tb[k], p, pinv);
+        aa[k] = r > rb ? aa[k] + ra : ra;
+        ab[k] = r > rb ? ab[k] + rb2 : rb2;
       }
     }
     __syncthreads();
+  }
+
+  if (a.acc_out) {  // representative split: hand this cluster's partial sums to the acc_in launch
+    uint4* dst = reinterpret_cast<uint4*>(
+        a.acc_out + (((size_t)row * (a.nsplit > 1 ? a.nsplit : 1) + split) * rc.np + PR) * 2 * N);
+    const uint4* src = reinterpret_cast<const uint4*>(S.acc);
+    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) dst[c] = src[c];
+    return;
   }
 
   // ---- inverse transforms of the two accumulators (buffers 0: a, 1: b) ----
@@ -575,6 +601,11 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 // a cluster processes SFHR_ROWS_PER_CLUSTER consecutive rows (twiddles staged once)
 template <int T, int A, int L, int PR>
 __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem) {
+  if (a.acc_out && a.nsplit > 1) {  // representative split: cluster = (row, split)
+    const int64_t cid = blockIdx.x / rc.np;
+    stage_row<T, A, L, PR>(rc, a, smem, cid / a.nsplit, true, (int)(cid % a.nsplit));
+    return;
+  }
   const int64_t row0 = (int64_t)(blockIdx.x / rc.np) * SFHR_ROWS_PER_CLUSTER;
   for (int rr = 0; rr < SFHR_ROWS_PER_CLUSTER; ++rr) {
     if (row0 + rr >= a.B) break;  // uniform across the cluster
@@ -692,7 +723,9 @@ static cudaError_t launch_stage_tal(const RingConst& rc, const StageArgs& a, cud
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((a.B + SFHR_ROWS_PER_CLUSTER - 1) / SFHR_ROWS_PER_CLUSTER * rc.np), 1, 1);
+  const int64_t clusters = a.acc_out && a.nsplit > 1 ? a.B * a.nsplit
+                                                     : (a.B + SFHR_ROWS_PER_CLUSTER - 1) / SFHR_ROWS_PER_CLUSTER;
+  cfg.gridDim = dim3((unsigned)(clusters * rc.np), 1, 1);
   cfg.blockDim = dim3(stage_threads(rc), 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

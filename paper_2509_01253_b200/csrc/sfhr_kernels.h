@@ -25,6 +25,12 @@ struct StageArgs {
   // ([B][np][2][N] u32, old NTT order, any value < 2^32) -> the kernel only runs the
   // inverse transforms, CRT and identity / body terms
   const uint32_t* acc_in;
+  // representative split (latency of small launches): with acc_out set, cluster (row, s) of a
+  // grid of B * nsplit clusters runs reps [s nreps / nsplit, (s + 1) nreps / nsplit) and writes
+  // its NTT-domain accumulators to acc_out [B][nsplit][np][2][N]; an acc_in launch with the same
+  // nsplit then sums the partials (0 or 1: one set)
+  uint32_t* acc_out;
+  int nsplit;
 };
 
 struct SpecArgs {
