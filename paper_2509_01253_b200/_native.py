@@ -113,11 +113,17 @@ class LinearDesc(C.Structure):
 
 # -- mirrors of the device constant block (debug / CPU verification only) --
 
+class WinoConst(C.Structure):
+    _fields_ = [("kT", C.c_uint64), ("kG", C.c_uint64), ("mu", C.c_uint32), ("rho", C.c_int32)] + \
+               [(n, C.c_int32) for n in ("a00", "a01", "a10", "b00", "b01", "b10")] + \
+               [(n, C.c_uint32) for n in ("k1p", "k2p", "k3p", "k4p", "k5p", "pad")]
+
+
 class PrimeConst(C.Structure):
     _fields_ = [("p", C.c_uint32), ("pinv", C.c_uint32), ("mu", C.c_uint32), ("r2", C.c_uint32),
                 ("rmod", C.c_uint32), ("z", (C.c_uint32 * 7) * 7), ("zi", (C.c_uint32 * 7) * 7),
                 ("g", (C.c_uint32 * 7) * 7), ("hc", (C.c_uint32 * 3) * 3), ("hs", (C.c_uint32 * 3) * 3),
-                ("q_mod64", C.c_uint64), ("inv_p", C.c_double)]
+                ("q_mod64", C.c_uint64), ("inv_p", C.c_double), ("wino", WinoConst * 2)]
 
 
 class RingConst(C.Structure):

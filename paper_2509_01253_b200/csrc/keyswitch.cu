@@ -119,22 +119,69 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
 #ifndef SFHR_SYM_DFT
 #define SFHR_SYM_DFT 1
 #endif
+#ifndef SFHR_WINO7
+#define SFHR_WINO7 1
+#endif
+
+// Rader/Winograd radix-7 DFT (constants and range proof: plan.cpp build_wino7).  The integer
+// multiply (fmaheavy) pipe bounds the stage kernel, so products are what to save: 10 IMAD.WIDE
+// + 6 REDC against 18 + 6 for dft_sym; the reconstruction adds run on the ALU pipe.
+// Inputs in [0, 2p); y_0 returned in [0, 2p), y_k < 2^32 (or [0, 2p) when RED).
+template <bool INV, bool RED>
+__device__ __forceinline__ void dft_wino7(const uint32_t (&x)[7], uint32_t (&y)[7], const PrimeConst& pc) {
+  const WinoConst& w = pc.wino[INV ? 1 : 0];
+  const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
+  // v_j = x_{5^j mod 7}
+  const uint32_t v0 = x[1], v1 = x[5], v2 = x[4], v3 = x[6], v4 = x[2], v5 = x[3];
+  const uint32_t p03 = v0 + v3, p14 = v1 + v4, p25 = v2 + v5;                       // [0, 4p)
+  const int32_t d03 = (int32_t)(v0 - v3), d14 = (int32_t)(v1 - v4), d25 = (int32_t)(v2 - v5);  // (-2p, 2p)
+  const uint32_t S = p03 + p14 + p25;                                               // V(1)
+  const int32_t Tm = d03 - d14 + d25;                                               // V(-1)
+  const int32_t A0 = (int32_t)(p03 - p25), A1 = (int32_t)(p14 - p25);               // V mod X^2+X+1
+  const int32_t C0 = d03 - d25, C1 = d14 + d25;                                     // V mod X^2-X+1
+  const uint32_t M0 = redc((uint64_t)S * w.mu, p, pinv);
+  const uint32_t R2 = redc((uint64_t)((int64_t)w.kT + (int64_t)Tm * w.rho), p, pinv);
+  const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
+  const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
+  const uint32_t h0 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b00 + (int64_t)C1 * w.b01), p, pinv);
+  const uint32_t h1 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b10 + (int64_t)C1 * w.b00), p, pinv);
+  // z_i = x_0 + M0 + (-1)^i R2 + g_{i mod 3} +- h_{i mod 3} (g_2 = -g_0 - g_1, h_2 = h_1 - h_0,
+  // h negated for i >= 3), mod 2^32 arithmetic whose true values are non-negative
+  const uint32_t X0 = x[0] + M0, Xp = X0 + R2, Xm = X0 - R2;
+  const uint32_t gs = g0 + g1, hd = h1 - h0;
+  uint32_t z[6];
+  z[0] = Xp + g0 + h0;
+  z[1] = Xm + w.k1p + g1 + h1;
+  z[2] = Xp + w.k3p - gs + hd;
+  z[3] = Xm + w.k2p + g0 - h0;
+  z[4] = Xp + w.k4p + g1 - h1;
+  z[5] = Xm + w.k5p - gs - hd;
+  const uint32_t y0 = x[0] + S;
+  y[0] = y0 - __umulhi(y0, mu) * p;
+  // outputs y_{3^i mod 7}
+  constexpr int kout[6] = {1, 3, 2, 6, 4, 5};
+#pragma unroll
+  for (int i = 0; i < 6; ++i) y[kout[i]] = RED ? z[i] - __umulhi(z[i], mu) * p : z[i];
+}
 
 // forward DFT whose k >= 1 outputs are multiplied by twiddles next (lazy [0, 6p) ok)
 template <int T>
 __device__ __forceinline__ void dft_fwd_tw(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
-  if (SFHR_SYM_DFT) dft_sym<T, false, false>(x, y, pc);
+  if constexpr (T == 7 && SFHR_WINO7) dft_wino7<false, false>(x, y, pc);
+  else if (SFHR_SYM_DFT) dft_sym<T, false, false>(x, y, pc);
   else dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
 }
 // forward / inverse DFT with every output in [0, 2p)
 template <int T>
 __device__ __forceinline__ void dft_fwd_red(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
-  if (SFHR_SYM_DFT) dft_sym<T, false, true>(x, y, pc);
+  if constexpr (T == 7 && SFHR_WINO7) dft_wino7<false, true>(x, y, pc);
+  else if (SFHR_SYM_DFT) dft_sym<T, false, true>(x, y, pc);
   else dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
 }
 template <int T>
 __device__ __forceinline__ void dft_inv_red(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
-  if (SFHR_SYM_DFT) dft_sym<T, true, true>(x, y, pc);
+  if constexpr (T == 7 && SFHR_WINO7) dft_wino7<true, true>(x, y, pc);
+  else if (SFHR_SYM_DFT) dft_sym<T, true, true>(x, y, pc);
   else dft_t<T>(x, y, pc.zi, pc.p, pc.pinv);
 }
 
@@ -415,7 +462,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 #pragma unroll
           for (int j = 0; j < T - 1; ++j) xv[j] = vals[j];
           xv[T - 1] = 0;
-          dft_sym<T, false, false>(xv, yq, pc);
+          dft_fwd_tw<T>(xv, yq, pc);
 #pragma unroll
           for (int q = 1; q < T; ++q) o[(q - 1) * n1] = mont_mul(yq[q], S.wt[q * m], p, pinv);
 #else

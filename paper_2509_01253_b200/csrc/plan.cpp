@@ -89,6 +89,63 @@ static long long tr_zeta(long long k, int t, int alpha) {
   return (k % n1 == 0) ? -n1 : 0;
 }
 
+// Rader/Winograd radix-7 DFT constants and range offsets (keyswitch.cu dft_wino7).  With
+// v_j = x_{5^j mod 7} and w_c = zeta^(3^c), y_{3^i} - x_0 = (v (*) w)_i (cyclic, length 6); the
+// product is computed from its residues mod X - 1 (W(1) = -1), X + 1, X^2 + X + 1 and
+// X^2 - X + 1 and reconstructed with 6 L^-1 (entries +-1, +-2; the 1/6 folded into constants).
+// Every bound below assumes inputs < 2p and is checked, so a prime that would overflow throws.
+static void build_wino7(PrimeConst& pc, uint64_t zeta, uint64_t p) {
+  const uint64_t R32 = 1ull << 32, Rm = R32 % p;
+  const uint64_t i6 = inv_mod(6 % p, p);
+  auto cen = [&](uint64_t v) -> int32_t {  // Montgomery form, centred
+    const uint64_t m = mulmod(v % p, Rm, p);
+    return m > p / 2 ? (int32_t)((int64_t)m - (int64_t)p) : (int32_t)m;
+  };
+  auto sub = [&](uint64_t a, uint64_t b) { return (a + p - b % p) % p; };
+  const long double X = 2.0L * p, ch = (long double)((p - 1) / 2), two32 = 4294967296.0L;
+  const long double Smax = 6.0L * X, Tmax = 3.0L * X, Amax = 2.0L * X;
+  for (int dir = 0; dir < 2; ++dir) {
+    const uint64_t z = dir ? inv_mod(zeta, p) : zeta;
+    uint64_t w[6];
+    for (int c = 0, g = 1; c < 6; ++c, g = g * 3 % 7) w[c] = powmod(z, (uint64_t)g, p);
+    const uint64_t B0 = sub((w[0] + w[3]) % p, (w[2] + w[5]) % p), B1 = sub((w[1] + w[4]) % p, (w[2] + w[5]) % p);
+    const uint64_t D0 = sub((w[0] + w[5]) % p, (w[3] + w[2]) % p), D1 = sub((w[1] + w[2]) % p, (w[4] + w[5]) % p);
+    uint64_t W1 = 0, Wm = 0;
+    for (int c = 0; c < 6; ++c) {
+      W1 = (W1 + w[c]) % p;
+      Wm = (c & 1) ? sub(Wm, w[c]) : (Wm + w[c]) % p;
+    }
+    WinoConst& k = pc.wino[dir];
+    std::memset(&k, 0, sizeof(k));
+    k.mu = (uint32_t)mulmod(mulmod(W1, i6, p), Rm, p);
+    k.rho = cen(mulmod(Wm, i6, p));
+    k.a00 = cen(mulmod(sub(2 * B0 % p, B1), i6, p));
+    k.a01 = cen(mulmod(sub(0, (B0 + B1) % p), i6, p));
+    k.a10 = cen(mulmod(sub(2 * B1 % p, B0), i6, p));
+    k.b00 = cen(mulmod((2 * D0 + D1) % p, i6, p));
+    k.b01 = cen(mulmod(sub(D0, D1), i6, p));
+    k.b10 = cen(mulmod((D0 + 2 * D1) % p, i6, p));
+    // REDC(x) <= floor(x / 2^32) + p; signed sums offset by a multiple of p
+    auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
+    k.kT = up(Tmax * ch);
+    k.kG = up(2.0L * Amax * ch);
+    const long double M0 = std::floor(Smax * (p - 1) / two32) + p;
+    const long double R2 = std::floor(((long double)k.kT + Tmax * ch) / two32) + p;
+    const long double G = std::floor(((long double)k.kG + 2.0L * Amax * ch) / two32) + p;
+    k.k1p = (uint32_t)up(R2);
+    k.k2p = (uint32_t)up(R2 + G);
+    k.k3p = (uint32_t)up(3.0L * G);
+    k.k4p = (uint32_t)up(G);
+    k.k5p = (uint32_t)up(R2 + 3.0L * G);
+    const long double X0 = X + M0;
+    const long double zmax[6] = {X0 + R2 + 2 * G, X0 + k.k1p + 2 * G, X0 + R2 + k.k3p + G,
+                                 X0 + k.k2p + G, X0 + R2 + k.k4p + G, X0 + k.k5p + G};
+    for (long double v : zmax)
+      if (v >= two32) throw std::invalid_argument("NTT prime too large for the radix-7 Winograd DFT ranges");
+    if (X + Smax >= two32) throw std::invalid_argument("NTT prime too large for the radix-7 DFT ranges");
+  }
+}
+
 Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) {
   if (t < 3 || !small_prime(t)) throw std::invalid_argument("t must be an odd prime >= 3");
   if (t != 3 && t != 5 && t != 7) throw std::invalid_argument("device kernels support t in {3, 5, 7}");
@@ -247,6 +304,7 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
           pc.hs[k - 1][m - 1] = mont(mulmod((zp + p - zm) % p, inv2, p));
         }
     }
+    if (t == 7) build_wino7(pc, zeta, p);
     // CRT: Q_i = P / p_i, Qinv = Q_i^-1 mod p_i
     uint64_t qmod64 = 1, qmodp = 1;
     for (int j = 0; j < rc.np; ++j)

@@ -21,6 +21,20 @@ constexpr int MAXL = 5;     // gadget depth
 constexpr int MAXREPS = 8;  // switched automorphisms per stage (t-1 <= 6)
 constexpr uint64_t QMASK = (1ull << 53) - 1;
 
+// Rader/Winograd radix-7 DFT (keyswitch.cu dft_wino7): the 6 nonzero inputs, reordered by
+// powers of the generator 3, form a length-6 cyclic convolution with the roots; it is split by
+// X^6 - 1 = (X - 1)(X + 1)(X^2 + X + 1)(X^2 - X + 1) into 10 products (vs 18 for the symmetric
+// pairs).  Constants in Montgomery form, signed ones centred in (-p/2, p/2); offsets keep every
+// REDC input and output sum non-negative and below 2^32 (bounds checked by the planner)
+struct WinoConst {
+  uint64_t kT, kG;      // multiples of p added to the signed R2 / g / h accumulations
+  uint32_t mu;          // W(1) / 6 * R in [0, p) (times the unsigned S)
+  int32_t rho;          // W(-1) / 6 * R
+  int32_t a00, a01, a10, b00, b01, b10;  // (X^2 + X + 1) / (X^2 - X + 1) parts, / 6, * R
+  uint32_t k1p, k2p, k3p, k4p, k5p;      // output-sum offsets (multiples of p)
+  uint32_t pad;
+};
+
 struct PrimeConst {
   uint32_t p;      // NTT prime, p = 1 mod M, p < 2^31 / max(t, l)
   uint32_t pinv;   // p^-1 mod 2^32
@@ -34,6 +48,7 @@ struct PrimeConst {
   uint32_t hs[MAXT / 2][MAXT / 2];  //                (zeta^(km) - zeta^(-km)) / 2 * R
   uint64_t q_mod64;         // (P / p) mod 2^64
   double inv_p;             // 1.0 / p
+  WinoConst wino[2];        // t = 7 only: forward, inverse
 };
 
 struct RingConst {

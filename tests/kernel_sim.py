@@ -3,8 +3,8 @@
 Replays, with the library's own constant tables (planning-only context, no
 GPU), exactly the arithmetic of ks_stage_kernel / ks_spectra_kernel in
 paper_2509_01253_b200/csrc/keyswitch.cu: Montgomery REDC with lazy [0, 2p)
-ranges, the symmetric-pair radix-t DFT (dft_sym, lazy [0, 6p) outputs before
-twiddles), the fused automorphism+decomposition first step, radix-t DIF/DIT
+ranges, the radix-t DFTs (Rader/Winograd dft_wino7 for t = 7, symmetric-pair dft_sym
+otherwise; lazy outputs before twiddles), the fused automorphism+decomposition first step, radix-t DIF/DIT
 stages, NTT-domain accumulation over reps, and explicit CRT mod 2^53.
 Every REDC input is range-checked, so an overflow in the kernel's bound
 reasoning fails here on CPU before any GPU time is spent.
@@ -59,6 +59,7 @@ class Prime:
         H = (T - 1) // 2
         self.hc = np.array([[pc.hc[k][m] for m in range(H)] for k in range(H)], dtype=U)
         self.hs = np.array([[pc.hs[k][m] for m in range(H)] for k in range(H)], dtype=U)
+        self.wino = [pc.wino[0], pc.wino[1]]
         self.q_mod64 = U(pc.q_mod64)
         self.inv_p = pc.inv_p
         self.wt = sp.tw[i]
@@ -130,10 +131,57 @@ class Prime:
             out[k], out[T - k] = (v, u) if inv else (u, v)
         return out
 
+    def dft_wino7(self, xs, inv=False, red=False):
+        """keyswitch.cu dft_wino7: Rader/Winograd radix-7 DFT, signed operands, its offsets."""
+        w = self.wino[1 if inv else 0]
+        p = int(self.p)
+        x = [np.asarray(v, dtype=U) for v in xs]
+        for v in x:
+            assert np.all(v < U(2 * p)), "DFT input >= 2p"
+        I = np.int64
+        v0, v1, v2, v3, v4, v5 = (x[i].astype(I) for i in (1, 5, 4, 6, 2, 3))
+        p03, p14, p25 = v0 + v3, v1 + v4, v2 + v5
+        d03, d14, d25 = v0 - v3, v1 - v4, v2 - v5
+        S = p03 + p14 + p25
+        Tm = d03 - d14 + d25
+        A0, A1 = p03 - p25, p14 - p25
+        C0, C1 = d03 - d25, d14 + d25
+        for a in (d03, d14, d25, Tm, A0, A1, C0, C1):
+            assert np.all(np.abs(a) < (1 << 31)), "signed 32-bit operand overflow"
+
+        def acc(off, *terms):
+            r = np.full(S.shape, off, dtype=I)
+            for a, c in terms:
+                r = r + a * I(c)
+            assert np.all(r >= 0), "negative REDC input"
+            return r.astype(U)
+        M0 = self.redc(S.astype(U) * U(w.mu))
+        R2 = self.redc(acc(w.kT, (Tm, w.rho)))
+        g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01)))
+        g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00)))
+        h0 = self.redc(acc(w.kG, (C0, w.b00), (C1, w.b01)))
+        h1 = self.redc(acc(w.kG, (C0, w.b10), (C1, w.b00)))
+        X0 = x[0].astype(I) + M0.astype(I)
+        R2, g0, g1, h0, h1 = (a.astype(I) for a in (R2, g0, g1, h0, h1))
+        gs, hd = g0 + g1, h1 - h0
+        z = [X0 + R2 + g0 + h0, X0 - R2 + w.k1p + g1 + h1, X0 + R2 + w.k3p - gs + hd,
+             X0 - R2 + w.k2p + g0 - h0, X0 + R2 + w.k4p + g1 - h1, X0 - R2 + w.k5p - gs - hd]
+        for a in z:
+            assert np.all(a >= 0) and np.all(a < (1 << 32)), "output sum out of [0, 2^32)"
+        out = [None] * 7
+        out[0] = self.barrett((x[0].astype(I) + S).astype(U))
+        for i, k in enumerate((1, 3, 2, 6, 4, 5)):
+            out[k] = self.barrett(z[i].astype(U)) if red else z[i].astype(U)
+        return out
+
+    def dft_k(self, xs, inv=False, red=False):
+        """The radix-t DFT the stage kernel uses for this ring (dft_fwd_tw / _red, dft_inv_red)."""
+        return self.dft_wino7(xs, inv, red) if len(xs) == 7 else self.dft_sym(xs, inv, red)
+
     def mont6(self, a, bm):
-        """mont_mul with a lazy [0, 6p) operand (twiddle after a symmetric DFT)."""
+        """mont_mul with a lazy operand (twiddle after a DFT: < 6p symmetric, < 2^32 Winograd)."""
         a = np.asarray(a, dtype=U)
-        assert np.all(a < U(6) * self.p)
+        assert np.all(a < U(1 << 32))
         return self.redc(a * np.asarray(bm, dtype=U))
 
 
@@ -143,7 +191,7 @@ def forward(sp: SimPlan, pr: Prime, vals):
     A = np.asarray(vals, dtype=U).reshape(T - 1, n1)
     m = np.arange(n1)
     buf = np.zeros((T - 1, n1), U)
-    ys = pr.dft_sym([A[j] for j in range(T - 1)] + [np.zeros(n1, U)])
+    ys = pr.dft_k([A[j] for j in range(T - 1)] + [np.zeros(n1, U)])
     for q in range(1, T):
         buf[q - 1] = pr.mont6(ys[q], pr.wt[q * m])
     buf = buf.reshape(-1)
@@ -155,7 +203,7 @@ def forward(sp: SimPlan, pr: Prime, vals):
         step = M // (T * L)
         j = np.arange(L)
         xs = [v[:, :, mm, :] for mm in range(T)]
-        ys = pr.dft_sym(xs)
+        ys = pr.dft_k(xs)
         nv = np.empty_like(v)
         nv[:, :, 0, :] = ys[0]
         for k in range(1, T):
@@ -163,14 +211,14 @@ def forward(sp: SimPlan, pr: Prime, vals):
         buf = nv.reshape(-1)
         L //= T
     x = buf.reshape(sp.nitems, T)
-    ys = pr.dft_sym([x[:, mm] for mm in range(T)], red=True)
+    ys = pr.dft_k([x[:, mm] for mm in range(T)], red=True)
     return np.stack(ys, axis=1)  # (nitems, T)
 
 
 def inverse(sp: SimPlan, pr: Prime, y):
     """y: (nitems, T) in [0,2p) -> (N,) CRT-weighted residues y_i in [0, p)."""
     T, n1, M = sp.t, sp.n1, sp.M
-    xs = pr.dft_sym([y[:, k] for k in range(T)], inv=True, red=True)
+    xs = pr.dft_k([y[:, k] for k in range(T)], inv=True, red=True)
     buf = np.stack(xs, axis=1).reshape(-1)
     L = T
     for s_ in range(sp.alpha - 3, -1, -1):
@@ -180,7 +228,7 @@ def inverse(sp: SimPlan, pr: Prime, y):
         j = np.arange(L)
         zs = [v[:, :, 0, :]] + [pr.mont(v[:, :, k, :], pr.wt[M - step * j * k][None, None, :])
                                for k in range(1, T)]
-        xs = pr.dft_sym(zs, inv=True, red=True)
+        xs = pr.dft_k(zs, inv=True, red=True)
         buf = np.stack(xs, axis=2).reshape(-1)
         L *= T
     v = buf.reshape(T - 1, n1)

@@ -128,6 +128,45 @@ def test_stage_kernel_arithmetic_simulation(t, alpha, b, gamma, D, l):
         sp.close()
 
 
+@pytest.mark.parametrize("gamma,D,l", [(0, 4096, 3), (1, 65536, 2)])
+def test_winograd_radix7_dft_exact_with_ranges(gamma, D, l):
+    """dft_wino7 (keyswitch.cu) with the library's constants: every output congruent to the
+    direct DFT, every REDC input / output sum inside the bounds the planner proved, for
+    random and extreme inputs < 2p, forward and inverse, lazy and reduced."""
+    import kernel_sim as ks
+    sp = ks.SimPlan(7, 4, 12, D, l, gamma)
+    try:
+        rng = np.random.default_rng(7)
+        for i in range(sp.np):
+            pr = ks.Prime(sp, i)
+            p = int(pr.p)
+            zeta = pow(_omega(p, sp.M), sp.M // 7, p)
+            xs = rng.integers(0, 2 * p, size=(7, 4096), dtype=np.int64).astype(np.uint64)
+            xs[:, :128] = rng.choice([0, 2 * p - 1], size=(7, 128)).astype(np.uint64)
+            xs[6, 128:256] = 0  # the fused first step's zero input
+            for inv in (False, True):
+                z = pow(zeta, -1, p) if inv else zeta
+                for red in (False, True):
+                    ys = pr.dft_k(list(xs), inv=inv, red=red)
+                    X = xs.astype(object)
+                    for k in range(7):
+                        want = sum(X[n] * pow(z, n * k, p) for n in range(7)) % p
+                        got = ys[k].astype(object) % p
+                        assert np.array_equal(got, want), (i, inv, red, k)
+                        if red or k == 0:
+                            assert np.all(ys[k] < 2 * p)
+    finally:
+        sp.close()
+
+
+def _omega(p, M):
+    """The planner's primitive M-th root (plan.cpp: first x whose (p-1)/M power has order M)."""
+    for x in range(2, p):
+        w = pow(x, (p - 1) // M, p)
+        if pow(w, M // 7, p) != 1:
+            return w
+
+
 @pytest.mark.parametrize("b,gamma", [(8, 0), (12, 0), (12, 1), (16, 0), (16, 1)])
 def test_closed_form_digits_match_reference_decomposition(b, gamma):
     """The device's per-digit closed forms (keyswitch.cu digit_i) with the library's
