@@ -122,6 +122,9 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
 #ifndef SFHR_WINO7
 #define SFHR_WINO7 1
 #endif
+#ifndef SFHR_WINO5
+#define SFHR_WINO5 1
+#endif
 
 // Rader/Winograd radix-7 DFT (constants and range proof: plan.cpp build_wino7).  The integer
 // multiply (fmaheavy) pipe bounds the stage kernel, so products are what to save: 10 IMAD.WIDE
@@ -165,9 +168,37 @@ __device__ __forceinline__ void dft_wino7(const uint32_t (&x)[7], uint32_t (&y)[
 }
 
 // forward DFT whose k >= 1 outputs are multiplied by twiddles next (lazy [0, 6p) ok)
+// Rader radix-5 DFT (plan.cpp build_wino5): 6 IMAD.WIDE + 4 REDC against 8 + 4 for dft_sym.
+// Inputs in [0, 2p); y_0 in [0, 2p), y_k < 2^32 (or [0, 2p) when RED).
+template <bool INV, bool RED>
+__device__ __forceinline__ void dft_wino5(const uint32_t (&x)[5], uint32_t (&y)[5], const PrimeConst& pc) {
+  const WinoConst& w = pc.wino[INV ? 1 : 0];
+  const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
+  const uint32_t v0 = x[1], v1 = x[3], v2 = x[4], v3 = x[2];  // v_j = x_{3^j mod 5}
+  const uint32_t S = v0 + v1 + v2 + v3;
+  const int32_t Tm = (int32_t)(v0 - v1 + v2 - v3);  // V(-1), (-4p, 4p)
+  const int32_t A0 = (int32_t)(v0 - v2), A1 = (int32_t)(v1 - v3);  // V mod X^2 + 1
+  const uint32_t M0 = redc((uint64_t)S * w.mu, p, pinv);
+  const uint32_t R2 = redc((uint64_t)((int64_t)w.kT + (int64_t)Tm * w.rho), p, pinv);
+  const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
+  const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
+  const uint32_t X0 = x[0] + M0, Xp = X0 + R2, Xm = X0 - R2;
+  uint32_t z[4];
+  z[0] = Xp + g0;
+  z[1] = Xm + w.k1p + g1;
+  z[2] = Xp + w.k2p - g0;
+  z[3] = Xm + w.k3p - g1;
+  const uint32_t y0 = x[0] + S;
+  y[0] = y0 - __umulhi(y0, mu) * p;
+  constexpr int kout[4] = {1, 2, 4, 3};  // outputs y_{2^i mod 5}
+#pragma unroll
+  for (int i = 0; i < 4; ++i) y[kout[i]] = RED ? z[i] - __umulhi(z[i], mu) * p : z[i];
+}
+
 template <int T>
 __device__ __forceinline__ void dft_fwd_tw(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
   if constexpr (T == 7 && SFHR_WINO7) dft_wino7<false, false>(x, y, pc);
+  else if constexpr (T == 5 && SFHR_WINO5) dft_wino5<false, false>(x, y, pc);
   else if (SFHR_SYM_DFT) dft_sym<T, false, false>(x, y, pc);
   else dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
 }
@@ -175,12 +206,14 @@ __device__ __forceinline__ void dft_fwd_tw(const uint32_t (&x)[T], uint32_t (&y)
 template <int T>
 __device__ __forceinline__ void dft_fwd_red(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
   if constexpr (T == 7 && SFHR_WINO7) dft_wino7<false, true>(x, y, pc);
+  else if constexpr (T == 5 && SFHR_WINO5) dft_wino5<false, true>(x, y, pc);
   else if (SFHR_SYM_DFT) dft_sym<T, false, true>(x, y, pc);
   else dft_t<T>(x, y, pc.z, pc.p, pc.pinv);
 }
 template <int T>
 __device__ __forceinline__ void dft_inv_red(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
   if constexpr (T == 7 && SFHR_WINO7) dft_wino7<true, true>(x, y, pc);
+  else if constexpr (T == 5 && SFHR_WINO5) dft_wino5<true, true>(x, y, pc);
   else if (SFHR_SYM_DFT) dft_sym<T, true, true>(x, y, pc);
   else dft_t<T>(x, y, pc.zi, pc.p, pc.pinv);
 }

@@ -146,6 +146,48 @@ static void build_wino7(PrimeConst& pc, uint64_t zeta, uint64_t p) {
   }
 }
 
+// Rader radix-5 DFT constants (keyswitch.cu dft_wino5): v_j = x_{3^j mod 5}, w_c = zeta^(2^c),
+// y_{2^i} - x_0 = (v (*) w)_i (cyclic, length 4) through X^4 - 1 = (X - 1)(X + 1)(X^2 + 1):
+// 6 products instead of 8.  Fields of WinoConst: mu = W(1)/4, rho = W(-1)/4, a00 = B0/2,
+// a01 = -B1/2, a10 = B1/2 (B = W mod X^2 + 1); k1p..k3p offsets of z1..z3.
+static void build_wino5(PrimeConst& pc, uint64_t zeta, uint64_t p) {
+  const uint64_t R32 = 1ull << 32, Rm = R32 % p;
+  const uint64_t i4 = inv_mod(4 % p, p), i2 = inv_mod(2 % p, p);
+  auto cen = [&](uint64_t v) -> int32_t {
+    const uint64_t m = mulmod(v % p, Rm, p);
+    return m > p / 2 ? (int32_t)((int64_t)m - (int64_t)p) : (int32_t)m;
+  };
+  auto sub = [&](uint64_t a, uint64_t b) { return (a + p - b % p) % p; };
+  const long double X = 2.0L * p, ch = (long double)((p - 1) / 2), two32 = 4294967296.0L;
+  for (int dir = 0; dir < 2; ++dir) {
+    const uint64_t z = dir ? inv_mod(zeta, p) : zeta;
+    uint64_t w[4];
+    for (int c = 0, g = 1; c < 4; ++c, g = g * 2 % 5) w[c] = powmod(z, (uint64_t)g, p);
+    const uint64_t B0 = sub(w[0], w[2]), B1 = sub(w[1], w[3]);
+    const uint64_t W1 = (w[0] + w[1] + w[2] + w[3]) % p, Wm = sub((w[0] + w[2]) % p, (w[1] + w[3]) % p);
+    WinoConst& k = pc.wino[dir];
+    std::memset(&k, 0, sizeof(k));
+    k.mu = (uint32_t)mulmod(mulmod(W1, i4, p), Rm, p);
+    k.rho = cen(mulmod(Wm, i4, p));
+    k.a00 = cen(mulmod(B0, i2, p));
+    k.a01 = cen(mulmod(sub(0, B1), i2, p));
+    k.a10 = cen(mulmod(B1, i2, p));
+    auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
+    k.kT = up(2.0L * X * ch);
+    k.kG = up(2.0L * X * ch);
+    const long double M0 = std::floor(4.0L * X * (p - 1) / two32) + p;
+    const long double R2 = std::floor(((long double)k.kT + 2.0L * X * ch) / two32) + p;
+    const long double G = std::floor(((long double)k.kG + 2.0L * X * ch) / two32) + p;
+    k.k1p = (uint32_t)up(R2);
+    k.k2p = (uint32_t)up(G);
+    k.k3p = (uint32_t)up(R2 + G);
+    const long double X0 = X + M0;
+    const long double zmax[4] = {X0 + R2 + G, X0 + k.k1p + G, X0 + R2 + k.k2p, X0 + k.k3p};
+    for (long double v : zmax)
+      if (v >= two32) throw std::invalid_argument("NTT prime too large for the radix-5 Rader DFT ranges");
+  }
+}
+
 Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) {
   if (t < 3 || !small_prime(t)) throw std::invalid_argument("t must be an odd prime >= 3");
   if (t != 3 && t != 5 && t != 7) throw std::invalid_argument("device kernels support t in {3, 5, 7}");
@@ -305,6 +347,7 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
         }
     }
     if (t == 7) build_wino7(pc, zeta, p);
+    if (t == 5) build_wino5(pc, zeta, p);
     // CRT: Q_i = P / p_i, Qinv = Q_i^-1 mod p_i
     uint64_t qmod64 = 1, qmodp = 1;
     for (int j = 0; j < rc.np; ++j)

@@ -3,8 +3,8 @@
 Replays, with the library's own constant tables (planning-only context, no
 GPU), exactly the arithmetic of ks_stage_kernel / ks_spectra_kernel in
 paper_2509_01253_b200/csrc/keyswitch.cu: Montgomery REDC with lazy [0, 2p)
-ranges, the radix-t DFTs (Rader/Winograd dft_wino7 for t = 7, symmetric-pair dft_sym
-otherwise; lazy outputs before twiddles), the fused automorphism+decomposition first step, radix-t DIF/DIT
+ranges, the radix-t DFTs (Rader/Winograd dft_wino7 / dft_wino5 for t = 7 / 5, symmetric-pair
+dft_sym for t = 3; lazy outputs before twiddles), the fused automorphism+decomposition first step, radix-t DIF/DIT
 stages, NTT-domain accumulation over reps, and explicit CRT mod 2^53.
 Every REDC input is range-checked, so an overflow in the kernel's bound
 reasoning fails here on CPU before any GPU time is spent.
@@ -174,9 +174,46 @@ class Prime:
             out[k] = self.barrett(z[i].astype(U)) if red else z[i].astype(U)
         return out
 
+    def dft_wino5(self, xs, inv=False, red=False):
+        """keyswitch.cu dft_wino5: Rader radix-5 DFT, signed operands, its offsets."""
+        w = self.wino[1 if inv else 0]
+        p = int(self.p)
+        x = [np.asarray(v, dtype=U) for v in xs]
+        for v in x:
+            assert np.all(v < U(2 * p)), "DFT input >= 2p"
+        I = np.int64
+        v0, v1, v2, v3 = (x[i].astype(I) for i in (1, 3, 4, 2))
+        S = v0 + v1 + v2 + v3
+        Tm = v0 - v1 + v2 - v3
+        A0, A1 = v0 - v2, v1 - v3
+
+        def acc(off, *terms):
+            r = np.full(S.shape, off, dtype=I)
+            for a, c in terms:
+                r = r + a * I(c)
+            assert np.all(r >= 0), "negative REDC input"
+            return r.astype(U)
+        M0 = self.redc(S.astype(U) * U(w.mu)).astype(I)
+        R2 = self.redc(acc(w.kT, (Tm, w.rho))).astype(I)
+        g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01))).astype(I)
+        g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00))).astype(I)
+        X0 = x[0].astype(I) + M0
+        z = [X0 + R2 + g0, X0 - R2 + w.k1p + g1, X0 + R2 + w.k2p - g0, X0 - R2 + w.k3p - g1]
+        for a in z:
+            assert np.all(a >= 0) and np.all(a < (1 << 32)), "output sum out of [0, 2^32)"
+        out = [None] * 5
+        out[0] = self.barrett((x[0].astype(I) + S).astype(U))
+        for i, k in enumerate((1, 2, 4, 3)):
+            out[k] = self.barrett(z[i].astype(U)) if red else z[i].astype(U)
+        return out
+
     def dft_k(self, xs, inv=False, red=False):
         """The radix-t DFT the stage kernel uses for this ring (dft_fwd_tw / _red, dft_inv_red)."""
-        return self.dft_wino7(xs, inv, red) if len(xs) == 7 else self.dft_sym(xs, inv, red)
+        if len(xs) == 7:
+            return self.dft_wino7(xs, inv, red)
+        if len(xs) == 5:
+            return self.dft_wino5(xs, inv, red)
+        return self.dft_sym(xs, inv, red)
 
     def mont6(self, a, bm):
         """mont_mul with a lazy operand (twiddle after a DFT: < 6p symmetric, < 2^32 Winograd)."""

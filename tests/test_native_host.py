@@ -128,29 +128,30 @@ def test_stage_kernel_arithmetic_simulation(t, alpha, b, gamma, D, l):
         sp.close()
 
 
-@pytest.mark.parametrize("gamma,D,l", [(0, 4096, 3), (1, 65536, 2)])
-def test_winograd_radix7_dft_exact_with_ranges(gamma, D, l):
-    """dft_wino7 (keyswitch.cu) with the library's constants: every output congruent to the
-    direct DFT, every REDC input / output sum inside the bounds the planner proved, for
+@pytest.mark.parametrize("t,alpha,b,gamma,D,l", [(7, 4, 12, 0, 4096, 3), (7, 4, 12, 1, 65536, 2),
+                                                  (5, 5, 16, 0, 310, 5), (5, 5, 16, 1, 310, 4)])
+def test_rader_dft_exact_with_ranges(t, alpha, b, gamma, D, l):
+    """dft_wino7 / dft_wino5 (keyswitch.cu) with the library's constants: every output congruent
+    to the direct DFT, every REDC input / output sum inside the bounds the planner proved, for
     random and extreme inputs < 2p, forward and inverse, lazy and reduced."""
     import kernel_sim as ks
-    sp = ks.SimPlan(7, 4, 12, D, l, gamma)
+    sp = ks.SimPlan(t, alpha, b, D, l, gamma)
     try:
         rng = np.random.default_rng(7)
         for i in range(sp.np):
             pr = ks.Prime(sp, i)
             p = int(pr.p)
-            zeta = pow(_omega(p, sp.M), sp.M // 7, p)
-            xs = rng.integers(0, 2 * p, size=(7, 4096), dtype=np.int64).astype(np.uint64)
-            xs[:, :128] = rng.choice([0, 2 * p - 1], size=(7, 128)).astype(np.uint64)
-            xs[6, 128:256] = 0  # the fused first step's zero input
+            zeta = pow(_omega(p, sp.M, t), sp.M // t, p)
+            xs = rng.integers(0, 2 * p, size=(t, 4096), dtype=np.int64).astype(np.uint64)
+            xs[:, :128] = rng.choice([0, 2 * p - 1], size=(t, 128)).astype(np.uint64)
+            xs[t - 1, 128:256] = 0  # the fused first step's zero input
             for inv in (False, True):
                 z = pow(zeta, -1, p) if inv else zeta
                 for red in (False, True):
                     ys = pr.dft_k(list(xs), inv=inv, red=red)
                     X = xs.astype(object)
-                    for k in range(7):
-                        want = sum(X[n] * pow(z, n * k, p) for n in range(7)) % p
+                    for k in range(t):
+                        want = sum(X[n] * pow(z, n * k, p) for n in range(t)) % p
                         got = ys[k].astype(object) % p
                         assert np.array_equal(got, want), (i, inv, red, k)
                         if red or k == 0:
@@ -159,11 +160,11 @@ def test_winograd_radix7_dft_exact_with_ranges(gamma, D, l):
         sp.close()
 
 
-def _omega(p, M):
+def _omega(p, M, t):
     """The planner's primitive M-th root (plan.cpp: first x whose (p-1)/M power has order M)."""
     for x in range(2, p):
         w = pow(x, (p - 1) // M, p)
-        if pow(w, M // 7, p) != 1:
+        if pow(w, M // t, p) != 1:
             return w
 
 
