@@ -125,6 +125,9 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
 #ifndef SFHR_WINO5
 #define SFHR_WINO5 1
 #endif
+#ifndef SFHR_WINO7_INV1
+#define SFHR_WINO7_INV1 1
+#endif
 
 // Rader/Winograd radix-7 DFT (constants and range proof: plan.cpp build_wino7).  The integer
 // multiply (fmaheavy) pipe bounds the stage kernel, so products are what to save: 10 IMAD.WIDE
@@ -168,6 +171,38 @@ __device__ __forceinline__ void dft_wino7(const uint32_t (&x)[7], uint32_t (&y)[
 }
 
 // forward DFT whose k >= 1 outputs are multiplied by twiddles next (lazy [0, 6p) ok)
+// Inverse first step of the t = 7 transform (plan.cpp build_wino7_invfirst): with Y the inverse
+// 7-point DFT of (0, C_1..C_6), out_j = s (Y_j - Y_6) = sum_r C_r g[j][r]; the Winograd form of
+// Y_j - Y_6 drops M0 and needs 10 products instead of the matrix's 36.  Inputs C < 2p; outputs
+// in [0, p) (the CRT-weighted residues).
+__device__ __forceinline__ void inv_first7(const uint32_t (&C)[6], uint32_t (&o)[6], const PrimeConst& pc) {
+  const WinoConst& w = pc.wino[2];
+  const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
+  // v_j = c_{5^j mod 7} with c_r = C[r - 1]
+  const uint32_t v0 = C[0], v1 = C[4], v2 = C[3], v3 = C[5], v4 = C[1], v5 = C[2];
+  const uint32_t p03 = v0 + v3, p14 = v1 + v4, p25 = v2 + v5;
+  const int32_t d03 = (int32_t)(v0 - v3), d14 = (int32_t)(v1 - v4), d25 = (int32_t)(v2 - v5);
+  const uint32_t S = p03 + p14 + p25;
+  const int32_t Tm = d03 - d14 + d25;
+  const int32_t A0 = (int32_t)(p03 - p25), A1 = (int32_t)(p14 - p25);
+  const int32_t C0 = d03 - d25, C1 = d14 + d25;
+  const uint32_t S7 = redc((uint64_t)S * w.mu, p, pinv);  // 7 s S / 6
+  const uint32_t R2 = redc((uint64_t)((int64_t)w.kT + (int64_t)Tm * w.rho), p, pinv);
+  const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
+  const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
+  const uint32_t h0 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b00 + (int64_t)C1 * w.b01), p, pinv);
+  const uint32_t h1 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b10 + (int64_t)C1 * w.b00), p, pinv);
+  uint32_t z[6];
+  z[0] = S7 + R2 + h0 + w.k1p - g0;
+  z[1] = 2 * (R2 + h0);
+  z[2] = 2 * R2 + h1 + w.k2p - 2 * g0 - g1;
+  z[3] = g1 + h1 + h0 + w.k3p - g0;
+  z[4] = 2 * R2 + g1 + h0 + w.k4p - h1 - g0;
+  z[5] = 2 * h0 + w.k5p - 2 * g0 - g1 - h1;
+#pragma unroll
+  for (int j = 0; j < 6; ++j) o[j] = fully(z[j] - __umulhi(z[j], mu) * p, p);
+}
+
 // Rader radix-5 DFT (plan.cpp build_wino5): 6 IMAD.WIDE + 4 REDC against 8 + 4 for dft_sym.
 // Inputs in [0, 2p); y_0 in [0, 2p), y_k < 2^32 (or [0, 2p) when RED).
 template <bool INV, bool RED>
@@ -348,12 +383,19 @@ __device__ __forceinline__ void inv_first_step(uint32_t* buf, int nb, const Ring
     uint32_t C[T - 1];
 #pragma unroll
     for (int r = 1; r < T; ++r) C[r - 1] = mont_mul(v[(r - 1) * g.n1], wt[g.M - r * m], pc.p, pc.pinv);
+    if constexpr (T == 7 && SFHR_WINO7 && SFHR_WINO7_INV1) {
+      uint32_t o[6];
+      inv_first7(C, o, pc);
 #pragma unroll
-    for (int j = 0; j < T - 1; ++j) {
-      uint64_t s = 0;
+      for (int j = 0; j < 6; ++j) v[j * g.n1] = o[j];
+    } else {
 #pragma unroll
-      for (int r = 0; r < T - 1; ++r) s += (uint64_t)C[r] * pc.g[j][r];
-      v[j * g.n1] = fully(redc(s, pc.p, pc.pinv), pc.p);
+      for (int j = 0; j < T - 1; ++j) {
+        uint64_t s = 0;
+#pragma unroll
+        for (int r = 0; r < T - 1; ++r) s += (uint64_t)C[r] * pc.g[j][r];
+        v[j * g.n1] = fully(redc(s, pc.p, pc.pinv), pc.p);
+      }
     }
   }
   __syncthreads();

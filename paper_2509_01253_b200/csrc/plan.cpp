@@ -4,6 +4,7 @@
 #include "plan.h"
 
 #include <cmath>
+#include <initializer_list>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -90,13 +91,17 @@ static long long tr_zeta(long long k, int t, int alpha) {
 }
 
 // Rader/Winograd radix-7 DFT constants and range offsets (keyswitch.cu dft_wino7).  With
-// v_j = x_{5^j mod 7} and w_c = zeta^(3^c), y_{3^i} - x_0 = (v (*) w)_i (cyclic, length 6); the
+// v_j = x_{5^j mod 7} and w_c = z^(3^c), y_{3^i} - x_0 = (v (*) w)_i (cyclic, length 6); the
 // product is computed from its residues mod X - 1 (W(1) = -1), X + 1, X^2 + X + 1 and
-// X^2 - X + 1 and reconstructed with 6 L^-1 (entries +-1, +-2; the 1/6 folded into constants).
-// Every bound below assumes inputs < 2p and is checked, so a prime that would overflow throws.
-static void build_wino7(PrimeConst& pc, uint64_t zeta, uint64_t p) {
+// X^2 - X + 1 and reconstructed with 6 L^-1 (entries +-1, +-2; the 1/6 folded into constants,
+// as is an optional output scale s).  Every bound below assumes inputs < 2p and is checked, so a
+// prime that would overflow throws.  Returns the REDC output bounds of M0, R2 and g / h.
+struct Wino7Bounds {
+  long double M0, R2, G;
+};
+static Wino7Bounds wino7_consts(WinoConst& k, uint64_t z, uint64_t scale, uint64_t p) {
   const uint64_t R32 = 1ull << 32, Rm = R32 % p;
-  const uint64_t i6 = inv_mod(6 % p, p);
+  const uint64_t i6 = mulmod(inv_mod(6 % p, p), scale % p, p);
   auto cen = [&](uint64_t v) -> int32_t {  // Montgomery form, centred
     const uint64_t m = mulmod(v % p, Rm, p);
     return m > p / 2 ? (int32_t)((int64_t)m - (int64_t)p) : (int32_t)m;
@@ -104,46 +109,75 @@ static void build_wino7(PrimeConst& pc, uint64_t zeta, uint64_t p) {
   auto sub = [&](uint64_t a, uint64_t b) { return (a + p - b % p) % p; };
   const long double X = 2.0L * p, ch = (long double)((p - 1) / 2), two32 = 4294967296.0L;
   const long double Smax = 6.0L * X, Tmax = 3.0L * X, Amax = 2.0L * X;
-  for (int dir = 0; dir < 2; ++dir) {
-    const uint64_t z = dir ? inv_mod(zeta, p) : zeta;
-    uint64_t w[6];
-    for (int c = 0, g = 1; c < 6; ++c, g = g * 3 % 7) w[c] = powmod(z, (uint64_t)g, p);
-    const uint64_t B0 = sub((w[0] + w[3]) % p, (w[2] + w[5]) % p), B1 = sub((w[1] + w[4]) % p, (w[2] + w[5]) % p);
-    const uint64_t D0 = sub((w[0] + w[5]) % p, (w[3] + w[2]) % p), D1 = sub((w[1] + w[2]) % p, (w[4] + w[5]) % p);
-    uint64_t W1 = 0, Wm = 0;
-    for (int c = 0; c < 6; ++c) {
-      W1 = (W1 + w[c]) % p;
-      Wm = (c & 1) ? sub(Wm, w[c]) : (Wm + w[c]) % p;
-    }
-    WinoConst& k = pc.wino[dir];
-    std::memset(&k, 0, sizeof(k));
-    k.mu = (uint32_t)mulmod(mulmod(W1, i6, p), Rm, p);
-    k.rho = cen(mulmod(Wm, i6, p));
-    k.a00 = cen(mulmod(sub(2 * B0 % p, B1), i6, p));
-    k.a01 = cen(mulmod(sub(0, (B0 + B1) % p), i6, p));
-    k.a10 = cen(mulmod(sub(2 * B1 % p, B0), i6, p));
-    k.b00 = cen(mulmod((2 * D0 + D1) % p, i6, p));
-    k.b01 = cen(mulmod(sub(D0, D1), i6, p));
-    k.b10 = cen(mulmod((D0 + 2 * D1) % p, i6, p));
-    // REDC(x) <= floor(x / 2^32) + p; signed sums offset by a multiple of p
-    auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
-    k.kT = up(Tmax * ch);
-    k.kG = up(2.0L * Amax * ch);
-    const long double M0 = std::floor(Smax * (p - 1) / two32) + p;
-    const long double R2 = std::floor(((long double)k.kT + Tmax * ch) / two32) + p;
-    const long double G = std::floor(((long double)k.kG + 2.0L * Amax * ch) / two32) + p;
-    k.k1p = (uint32_t)up(R2);
-    k.k2p = (uint32_t)up(R2 + G);
-    k.k3p = (uint32_t)up(3.0L * G);
-    k.k4p = (uint32_t)up(G);
-    k.k5p = (uint32_t)up(R2 + 3.0L * G);
-    const long double X0 = X + M0;
-    const long double zmax[6] = {X0 + R2 + 2 * G, X0 + k.k1p + 2 * G, X0 + R2 + k.k3p + G,
-                                 X0 + k.k2p + G, X0 + R2 + k.k4p + G, X0 + k.k5p + G};
-    for (long double v : zmax)
-      if (v >= two32) throw std::invalid_argument("NTT prime too large for the radix-7 Winograd DFT ranges");
-    if (X + Smax >= two32) throw std::invalid_argument("NTT prime too large for the radix-7 DFT ranges");
+  uint64_t w[6];
+  for (int c = 0, g = 1; c < 6; ++c, g = g * 3 % 7) w[c] = powmod(z, (uint64_t)g, p);
+  const uint64_t B0 = sub((w[0] + w[3]) % p, (w[2] + w[5]) % p), B1 = sub((w[1] + w[4]) % p, (w[2] + w[5]) % p);
+  const uint64_t D0 = sub((w[0] + w[5]) % p, (w[3] + w[2]) % p), D1 = sub((w[1] + w[2]) % p, (w[4] + w[5]) % p);
+  uint64_t W1 = 0, Wm = 0;
+  for (int c = 0; c < 6; ++c) {
+    W1 = (W1 + w[c]) % p;
+    Wm = (c & 1) ? sub(Wm, w[c]) : (Wm + w[c]) % p;
   }
+  std::memset(&k, 0, sizeof(k));
+  k.mu = (uint32_t)mulmod(mulmod(W1, i6, p), Rm, p);
+  k.rho = cen(mulmod(Wm, i6, p));
+  k.a00 = cen(mulmod(sub(2 * B0 % p, B1), i6, p));
+  k.a01 = cen(mulmod(sub(0, (B0 + B1) % p), i6, p));
+  k.a10 = cen(mulmod(sub(2 * B1 % p, B0), i6, p));
+  k.b00 = cen(mulmod((2 * D0 + D1) % p, i6, p));
+  k.b01 = cen(mulmod(sub(D0, D1), i6, p));
+  k.b10 = cen(mulmod((D0 + 2 * D1) % p, i6, p));
+  // REDC(x) <= floor(x / 2^32) + p; signed sums offset by a multiple of p
+  auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
+  k.kT = up(Tmax * ch);
+  k.kG = up(2.0L * Amax * ch);
+  if (X + Smax >= two32) throw std::invalid_argument("NTT prime too large for the radix-7 DFT ranges");
+  return {std::floor(Smax * (p - 1) / two32) + p, std::floor(((long double)k.kT + Tmax * ch) / two32) + p,
+          std::floor(((long double)k.kG + 2.0L * Amax * ch) / two32) + p};
+}
+
+static uint32_t up_p(long double v, uint64_t p) { return (uint32_t)((uint64_t)std::ceil(v / (long double)p) * p); }
+
+static void check32(std::initializer_list<long double> maxima) {
+  for (long double v : maxima)
+    if (v >= 4294967296.0L) throw std::invalid_argument("NTT prime too large for the radix-7 Winograd DFT ranges");
+}
+
+// forward (wino[0]) and inverse (wino[1]) radix-7 DFTs
+static void build_wino7(PrimeConst& pc, uint64_t zeta, uint64_t p) {
+  const long double X = 2.0L * p;
+  for (int dir = 0; dir < 2; ++dir) {
+    WinoConst& k = pc.wino[dir];
+    const Wino7Bounds b = wino7_consts(k, dir ? inv_mod(zeta, p) : zeta, 1, p);
+    const long double R2 = b.R2, G = b.G;
+    k.k1p = up_p(R2, p);
+    k.k2p = up_p(R2 + G, p);
+    k.k3p = up_p(3.0L * G, p);
+    k.k4p = up_p(G, p);
+    k.k5p = up_p(R2 + 3.0L * G, p);
+    const long double X0 = X + b.M0;
+    check32({X0 + R2 + 2 * G, X0 + k.k1p + 2 * G, X0 + R2 + k.k3p + G, X0 + k.k2p + G, X0 + R2 + k.k4p + G,
+             X0 + k.k5p + G});
+  }
+}
+
+// inverse first step (wino[2], keyswitch.cu inv_first7): out_j = s (Y_j - Y_6), j < 6, where Y is
+// the inverse 7-point DFT of (0, C_1..C_6) and s = Qinv / M (the CRT weight; pc.g's matrix is
+// s (zeta^-rj - zeta^r)).  Constants scaled by s; mu holds 7 s / 6 (out_0 = 7 s S / 6 + ...),
+// k1p..k5p offset out_0, out_2, out_3, out_4, out_5.
+static void build_wino7_invfirst(PrimeConst& pc, uint64_t zeta, uint64_t s, uint64_t p) {
+  WinoConst& k = pc.wino[2];
+  const Wino7Bounds b = wino7_consts(k, inv_mod(zeta, p), s, p);
+  const uint64_t Rm = (1ull << 32) % p;
+  k.mu = (uint32_t)mulmod(mulmod(mulmod(7, inv_mod(6, p), p), s, p), Rm, p);
+  const long double R2 = b.R2, G = b.G, S7 = b.M0;
+  k.k1p = up_p(G, p);
+  k.k2p = up_p(3.0L * G, p);
+  k.k3p = up_p(G, p);
+  k.k4p = up_p(2.0L * G, p);
+  k.k5p = up_p(4.0L * G, p);
+  check32({S7 + R2 + G + k.k1p, 2 * R2 + 2 * G, 2 * R2 + 2 * G + k.k2p, 3 * G + k.k3p, 2 * R2 + 2 * G + k.k4p,
+           3 * G + k.k5p});
 }
 
 // Rader radix-5 DFT constants (keyswitch.cu dft_wino5): v_j = x_{3^j mod 5}, w_c = zeta^(2^c),
@@ -359,6 +393,7 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
     pc.inv_p = 1.0 / (double)p;
     const uint64_t qinv = inv_mod(qmodp, p);
     const uint64_t minv = inv_mod((uint64_t)M % p, p);
+    if (t == 7) build_wino7_invfirst(pc, zeta, mulmod(minv, qinv, p), p);
     for (int j = 0; j < t - 1; ++j)
       for (int r = 1; r < t; ++r) {
         uint64_t a = powmod(zeta, (uint64_t)((t - (r * j) % t) % t), p);

@@ -48,7 +48,7 @@ struct PrimeConst {
   uint32_t hs[MAXT / 2][MAXT / 2];  //                (zeta^(km) - zeta^(-km)) / 2 * R
   uint64_t q_mod64;         // (P / p) mod 2^64
   double inv_p;             // 1.0 / p
-  WinoConst wino[2];        // t = 7 only: forward, inverse
+  WinoConst wino[3];        // t = 7: forward, inverse, inverse first step (t = 5: [0], [1])
 };
 
 struct RingConst {

@@ -59,7 +59,7 @@ class Prime:
         H = (T - 1) // 2
         self.hc = np.array([[pc.hc[k][m] for m in range(H)] for k in range(H)], dtype=U)
         self.hs = np.array([[pc.hs[k][m] for m in range(H)] for k in range(H)], dtype=U)
-        self.wino = [pc.wino[0], pc.wino[1]]
+        self.wino = [pc.wino[0], pc.wino[1], pc.wino[2]]
         self.q_mod64 = U(pc.q_mod64)
         self.inv_p = pc.inv_p
         self.wt = sp.tw[i]
@@ -207,6 +207,42 @@ class Prime:
             out[k] = self.barrett(z[i].astype(U)) if red else z[i].astype(U)
         return out
 
+    def inv_first7(self, Cs):
+        """keyswitch.cu inv_first7: the t = 7 inverse first step in Winograd form -> [0, p)."""
+        w = self.wino[2]
+        p = int(self.p)
+        I = np.int64
+        for c in Cs:
+            assert np.all(np.asarray(c) < U(2 * p))
+        c = [np.asarray(x, dtype=U).astype(I) for x in Cs]
+        v0, v1, v2, v3, v4, v5 = c[0], c[4], c[3], c[5], c[1], c[2]
+        p03, p14, p25 = v0 + v3, v1 + v4, v2 + v5
+        d03, d14, d25 = v0 - v3, v1 - v4, v2 - v5
+        S = p03 + p14 + p25
+        Tm = d03 - d14 + d25
+        A0, A1, C0, C1 = p03 - p25, p14 - p25, d03 - d25, d14 + d25
+
+        def acc(off, *terms):
+            r = np.full(S.shape, off, dtype=I)
+            for a, k in terms:
+                r = r + a * I(k)
+            assert np.all(r >= 0)
+            return r.astype(U)
+        S7 = self.redc(S.astype(U) * U(w.mu)).astype(I)
+        R2 = self.redc(acc(w.kT, (Tm, w.rho))).astype(I)
+        g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01))).astype(I)
+        g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00))).astype(I)
+        h0 = self.redc(acc(w.kG, (C0, w.b00), (C1, w.b01))).astype(I)
+        h1 = self.redc(acc(w.kG, (C0, w.b10), (C1, w.b00))).astype(I)
+        z = [S7 + R2 + h0 + w.k1p - g0, 2 * (R2 + h0), 2 * R2 + h1 + w.k2p - 2 * g0 - g1,
+             g1 + h1 + h0 + w.k3p - g0, 2 * R2 + g1 + h0 + w.k4p - h1 - g0, 2 * h0 + w.k5p - 2 * g0 - g1 - h1]
+        out = []
+        for a in z:
+            assert np.all(a >= 0) and np.all(a < (1 << 32)), "inverse first step sum out of range"
+            r = self.barrett(a.astype(U))
+            out.append(np.where(r >= self.p, r - self.p, r))
+        return np.stack(out)
+
     def dft_k(self, xs, inv=False, red=False):
         """The radix-t DFT the stage kernel uses for this ring (dft_fwd_tw / _red, dft_inv_red)."""
         if len(xs) == 7:
@@ -271,6 +307,8 @@ def inverse(sp: SimPlan, pr: Prime, y):
     v = buf.reshape(T - 1, n1)
     m = np.arange(n1)
     Cs = [pr.mont(v[r - 1], pr.wt[M - r * m]) for r in range(1, T)]
+    if T == 7:
+        return pr.inv_first7(Cs).reshape(-1)
     out = np.zeros((T - 1, n1), U)
     for j in range(T - 1):
         s = np.zeros(n1, U)

@@ -160,6 +160,30 @@ def test_rader_dft_exact_with_ranges(t, alpha, b, gamma, D, l):
         sp.close()
 
 
+@pytest.mark.parametrize("gamma,D,l", [(0, 4096, 3), (1, 65536, 2)])
+def test_winograd_inverse_first_step_matches_matrix(gamma, D, l):
+    """inv_first7 (keyswitch.cu, t = 7) equals the (t-1)x(t-1) CRT-weighted solve sum_r C_r g[j][r]
+    it replaces, fully reduced, for random and extreme inputs < 2p."""
+    import kernel_sim as ks
+    sp = ks.SimPlan(7, 4, 12, D, l, gamma)
+    try:
+        rng = np.random.default_rng(11)
+        for i in range(sp.np):
+            pr = ks.Prime(sp, i)
+            p = int(pr.p)
+            Cs = rng.integers(0, 2 * p, size=(6, 2048), dtype=np.int64).astype(np.uint64)
+            Cs[:, :64] = rng.choice([0, 2 * p - 1], size=(6, 64)).astype(np.uint64)
+            got = pr.inv_first7(list(Cs))
+            R_inv = pow(1 << 32, -1, p)
+            G = pr.g.astype(object)
+            X = Cs.astype(object)
+            for j in range(6):
+                want = sum(X[r] * G[j][r] for r in range(6)) * R_inv % p
+                assert np.array_equal(got[j].astype(object), want), (i, j)
+    finally:
+        sp.close()
+
+
 def _omega(p, M, t):
     """The planner's primitive M-th root (plan.cpp: first x whose (p-1)/M power has order M)."""
     for x in range(2, p):
