@@ -308,7 +308,7 @@ def run_ours(args, rank, world, local_rank):
             "launches_timed": ks_launches, "kernel_ms_per_step": ks_ms / args.steps,
             "kernel_share_of_step": (ks_ms / total_ms) if total_ms else None,
             "peak_source": "MEASURED_PEAKS.json" if PEAKS.exists() else "fallback 6650 GB/s",
-            "note": "INT-pipe bound at these ring sizes (SURVEY §8(d)); HBM fraction reported as required"}
+            "note": "bound by the integer-multiply (fmaheavy) pipe at these ring sizes, see traffic_detail.int_mul_pipe_busy_frac (SURVEY §8(d)); HBM fraction reported as required"}
 
     line = {
         "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -335,7 +335,7 @@ def stage_traffic(N):
     algorithmic 32 N bytes per row (rows = grid / 3 CTAs per cluster); the capture
     is of the b = 12 (N = 2058) ResNet-20 stem pack, so the ratio is only quoted
     for that ring."""
-    f = ROOT / "profiles" / "r02_ncu_stage_summary.json"
+    f = ROOT / "profiles" / "r02_ncu_stage_final_summary.json"
     try:
         launches = [l for l in json.loads(f.read_text())["launches"] if "ks_stage_kernel" in l["kernel"]]
     except Exception:
@@ -344,13 +344,14 @@ def stage_traffic(N):
     alg = [l["launch__grid_size"] / 3 * 32 * 2058 for l in launches]
     out = {"traffic": sum(tr) / len(tr), "unit": "bytes per launch", "launches": len(tr),
            "algorithmic_bytes_per_launch": sum(alg) / len(alg), "source": f"profiles/{f.name}"}
-    # the compute side of the same capture: this kernel is issue/latency bound, not HBM bound
+    # the compute side of the same capture: this kernel is bound by the integer-multiply pipe
+    # (IMAD / IMAD.HI / IMAD.WIDE run only on fmaheavy), not by HBM
     def mean(key):
         v = [l.get(key) for l in launches if isinstance(l.get(key), float)]
         return sum(v) / len(v) / 100.0 if v else None
+    out["int_mul_pipe_busy_frac"] = mean("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed")
+    out["alu_pipe_busy_frac"] = mean("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active")
     out["sm_issue_active_frac"] = mean("smsp__issue_active.avg.pct_of_peak_sustained_active")
-    out["fma_pipe_frac"] = mean("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active")
-    out["alu_pipe_frac"] = mean("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active")
     if N == 2058:
         out["traffic_over_algorithmic"] = sum(tr) / sum(alg)
     return out

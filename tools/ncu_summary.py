@@ -19,7 +19,11 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
            "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
-           "l1tex__m_xbar2l1tex_read_bytes.sum"]
+           "l1tex__m_xbar2l1tex_read_bytes.sum",
+           # busy cycles (not instruction counts): IMAD / IMAD.HI / IMAD.WIDE issue only to fmaheavy
+           "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"]
 rep, out = sys.argv[1], sys.argv[2]
 txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
                      capture_output=True, text=True).stdout
