@@ -47,6 +47,9 @@ struct sfhr_ctx {
   uint32_t* tc_ws = nullptr;  // NTT-domain accumulator workspace (grow-only), last used on ...
   size_t tc_ws_bytes = 0;
   cudaEvent_t tc_ws_free = nullptr;  // ... the stream position recorded here
+  uint32_t* crt_ws = nullptr;  // L2 CRT residues + row counters (grow-only), same protocol
+  size_t crt_ws_bytes = 0;
+  cudaEvent_t crt_ws_free = nullptr;
   std::mutex mu;
 };
 
@@ -140,20 +143,88 @@ int rep_split(int nreps, int64_t B) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(nreps, want));
 }
 
-// grow-only device workspace of a context, shared by the tensor-core and representative-split
-// paths; a call waits (stream-ordered) for the previous user recorded on tc_ws_free
-int workspace(sfhr_ctx* ctx, size_t bytes, cudaStream_t st, uint32_t** out) {
-  if (!ctx->tc_ws_free) CK(cudaEventCreateWithFlags(&ctx->tc_ws_free, cudaEventDisableTiming), "workspace event");
-  if (bytes > ctx->tc_ws_bytes) {  // grow (rare): wait for the last user before freeing
-    CK(cudaEventSynchronize(ctx->tc_ws_free), "workspace sync");
-    cudaFree(ctx->tc_ws);
-    ctx->tc_ws = nullptr;
-    ctx->tc_ws_bytes = 0;
-    CK(cudaMalloc(reinterpret_cast<void**>(&ctx->tc_ws), bytes), "workspace alloc");
-    ctx->tc_ws_bytes = bytes;
+// grow-only device workspace; a call waits (stream-ordered) for the previous user recorded on
+// its event
+int grow_workspace(uint32_t*& buf, size_t& have, cudaEvent_t& ev, size_t bytes, cudaStream_t st, uint32_t** out) {
+  if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "workspace event");
+  if (bytes > have) {  // grow (rare): wait for the last user before freeing
+    CK(cudaEventSynchronize(ev), "workspace sync");
+    cudaFree(buf);
+    buf = nullptr;
+    have = 0;
+    CK(cudaMalloc(reinterpret_cast<void**>(&buf), bytes), "workspace alloc");
+    have = bytes;
   }
-  CK(cudaStreamWaitEvent(st, ctx->tc_ws_free, 0), "workspace wait");  // a previous caller's stream
-  *out = ctx->tc_ws;
+  CK(cudaStreamWaitEvent(st, ev, 0), "workspace wait");  // a previous caller's stream
+  *out = buf;
+  return SFHR_OK;
+}
+
+// the context's accumulator workspace, shared by the tensor-core and representative-split paths
+int workspace(sfhr_ctx* ctx, size_t bytes, cudaStream_t st, uint32_t** out) {
+  return grow_workspace(ctx->tc_ws, ctx->tc_ws_bytes, ctx->tc_ws_free, bytes, st, out);
+}
+
+// Stage launches finish with the explicit CRT of each row over its np prime CTAs.  Default
+// (SFHR_STAGE_CLUSTER unset or 0): independent CTAs and a CRT through L2 (crt_scratch, last
+// arriver); SFHR_STAGE_CLUSTER=1: the CTAs of a row form a thread-block cluster and exchange
+// residues through distributed shared memory.  Clusters of 3 CTAs leave 4 % of the CTA slots
+// of a B200 unusable (cudaOccupancyMaxActiveClusters: 142 x 3 of 148 x 3) and make every CTA
+// wait for its slowest peer.
+bool stage_clusters() {
+  static const bool on = [] {
+    const char* e = std::getenv("SFHR_STAGE_CLUSTER");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// launches with fewer rows than this keep the cluster CRT: they are latency bound, and the L2
+// CRT's last arriver serialises the whole row's CRT (SFHR_CRT_MIN_ROWS, default one row per SM)
+int64_t crt_min_rows() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("SFHR_CRT_MIN_ROWS");
+    if (e) return (int64_t)std::atoll(e);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return (int64_t)nsm;
+  }();
+  return v;
+}
+
+// launch a stage (or the acc_in tail of a split / tensor-core stage) with the configured CRT;
+// rows go in chunks so that the CRT scratch stays a few hundred MB
+constexpr int64_t CRT_CHUNK_ROWS = 8192;
+int launch_stage_crt(sfhr_ctx* ctx, const StageArgs& a, cudaStream_t st, const char* what) {
+  const RingConst& rc = ctx->plan.rc;
+  if (stage_clusters() || a.B < crt_min_rows()) {
+    CK(launch_stage(rc, a, st), what);
+    return SFHR_OK;
+  }
+  const size_t row_words = crt_row_words(rc);
+  const int64_t chunk = std::min<int64_t>(a.B, CRT_CHUNK_ROWS);
+  const size_t scratch_bytes = (size_t)chunk * row_words * 4;
+  uint32_t* ws = nullptr;
+  if (const int rc_ = grow_workspace(ctx->crt_ws, ctx->crt_ws_bytes, ctx->crt_ws_free,
+                                     scratch_bytes + (size_t)chunk * 4, st, &ws))
+    return rc_;
+  unsigned* cnt = reinterpret_cast<unsigned*>(ws + (size_t)chunk * row_words);
+  const int parts = a.nsplit > 1 ? a.nsplit : 1;
+  for (int64_t r0 = 0; r0 < a.B; r0 += chunk) {
+    StageArgs c = a;
+    c.B = std::min<int64_t>(chunk, a.B - r0);
+    c.in = a.in + r0 * 2 * rc.N;
+    c.out = a.out + r0 * 2 * rc.N;
+    if (a.acc_in) c.acc_in = a.acc_in + (size_t)r0 * parts * rc.np * 2 * rc.N;
+    c.independent = 1;
+    c.crt_scratch = ws;
+    c.crt_cnt = cnt;
+    CK(cudaMemsetAsync(cnt, 0, (size_t)c.B * 4, st), "CRT counters");
+    CK(launch_stage(rc, c, st), what);
+    if (r0) ++g_launches;  // the callers count one launch per stage
+  }
+  CK(cudaEventRecord(ctx->crt_ws_free, st), "CRT workspace release");
   return SFHR_OK;
 }
 
@@ -287,7 +358,7 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
       t.out = out + r0 * 2 * P.rc.N;
       t.B = nb;
       t.acc_in = acc;
-      CK(launch_stage(P.rc, t, st), "stage kernel (inverse / CRT)");
+      if (const int rc_ = launch_stage_crt(ctx, t, st, "stage kernel (inverse / CRT)")) return rc_;
       g_launches += 3;
     }
     CK(cudaEventRecord(ctx->tc_ws_free, st), "tc workspace release");
@@ -301,15 +372,16 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     StageArgs s1 = a;
     s1.acc_out = ws;
     s1.nsplit = split;
+    s1.independent = 1;  // no CRT in this half: its CTAs never talk to each other
     CK(launch_stage(P.rc, s1, st), "stage kernel (representative split)");
     StageArgs s2 = a;
     s2.acc_in = ws;
     s2.nsplit = split;
-    CK(launch_stage(P.rc, s2, st), "stage kernel (inverse / CRT)");
+    if (const int rc_ = launch_stage_crt(ctx, s2, st, "stage kernel (inverse / CRT)")) return rc_;
     CK(cudaEventRecord(ctx->tc_ws_free, st), "workspace release");
     ++g_launches;
   } else {
-    CK(launch_stage(P.rc, a, st), "stage kernel");
+    if (const int rc_ = launch_stage_crt(ctx, a, st, "stage kernel")) return rc_;
   }
   if (g_debug_sync) {  // SFHR_DEBUG_SYNC=1: locate a faulting launch
     cudaError_t e = cudaStreamSynchronize(st);
@@ -428,6 +500,9 @@ int sfhr_ctx_destroy(sfhr_ctx* ctx) {
   if (ctx->tc_ws_free) cudaEventSynchronize(ctx->tc_ws_free);
   cudaFree(ctx->tc_ws);
   if (ctx->tc_ws_free) cudaEventDestroy(ctx->tc_ws_free);
+  if (ctx->crt_ws_free) cudaEventSynchronize(ctx->crt_ws_free);
+  cudaFree(ctx->crt_ws);
+  if (ctx->crt_ws_free) cudaEventDestroy(ctx->crt_ws_free);
   delete ctx;
   return SFHR_OK;
 }

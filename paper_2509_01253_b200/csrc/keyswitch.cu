@@ -500,7 +500,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       }
       dst[c] = v;
     }
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (!a.independent) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     __syncthreads();
   }
   for (int r = rb; r < (a.acc_in ? rb : re); ++r) {
@@ -573,7 +573,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     fwd_mid_stages<T, A, PR>(S.buf, L, rc, S.wt);
     // the staged mask is dead after the last rep's gathers: tell the peers they may push
     // their CRT residues into it (the matching wait precedes our own pushes)
-    if (r == a.nreps - 1 && !a.acc_out) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+    if (r == a.nreps - 1 && !a.independent) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     // ---- C: last stage (span 1) in registers, MAC against the key spectra ----
     if (owner) {
       const uint32_t* ks = a.spec[r];
@@ -637,10 +637,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   inv_mid_stages<T, A, PR>(S.buf, 2, rc, S.wt);
   inv_first_step<T, A, PR>(S.buf, 2, rc, S.wt);
 
-  // ---- body term sum_r aut_r(x.b) of this CTA's slice, gathered from global into the
-  // (now free) accumulator region while the other CTAs of the cluster finish ----
-  uint64_t* bsum_s = reinterpret_cast<uint64_t*>(S.acc);  // (k1 - k0) u64 <= N u64
-  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+  // body term x.b + sum_r aut_r(x.b) of coefficient k, gathered from global
+  auto body_sum = [&](const int k) -> uint64_t {
     uint64_t bsum = a.identity ? xin[N + k] : 0ull;
     const uint32_t kmod = (uint32_t)(k % n1);
 #if SFHR_BODY_UNROLL
@@ -671,8 +669,66 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       bsum += v;
     }
 #endif
-    bsum_s[k - k0] = bsum;
+    return bsum;
+  };
+  // explicit CRT of coefficient k from the np CRT-weighted residues (ya_i, yb_i)
+  auto crt_out = [&](const int k, const uint32_t* ya, const uint32_t* yb, const uint64_t bsum) {
+    uint64_t ua = 0, ub = 0;
+    double fa = 0.0, fb = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXNP; ++i) {
+      if (i < rc.np) {
+        ua += (uint64_t)ya[i] * rc.pc[i].q_mod64;
+        ub += (uint64_t)yb[i] * rc.pc[i].q_mod64;
+        fa += (double)ya[i] * rc.pc[i].inv_p;
+        fb += (double)yb[i] * rc.pc[i].inv_p;
+      }
+    }
+    const uint64_t Av = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
+    const uint64_t Bv = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
+    xout[k] = ((a.identity ? xin[k] : 0ull) - Av) & QMASK;
+    xout[N + k] = (bsum - Bv) & QMASK;
+  };
+
+  if (a.crt_scratch) {
+    // ---- CRT through L2 (independent CTAs, no cluster): every CTA stores its residues of the
+    // whole row, and the last of the row's np CTAs to arrive (device-scope counter) combines
+    // them, adds the body term and writes the row; the others exit at once ----
+    uint32_t* rs = a.crt_scratch + (size_t)row * crt_row_words(rc);
+    {
+      uint4* mine = reinterpret_cast<uint4*>(rs + (size_t)PR * 2 * N);
+      const uint4* src = reinterpret_cast<const uint4*>(S.buf);
+      for (int c = threadIdx.x; c < N / 2; c += blockDim.x) mine[c] = src[c];  // 2N u32
+    }
+    __threadfence();
+    __syncthreads();
+    uint32_t* flag = reinterpret_cast<uint32_t*>(S.acc);  // free after the inverse transforms
+    if (threadIdx.x == 0) flag[0] = atomicAdd(a.crt_cnt + row, 1u) == (unsigned)(rc.np - 1);
+    __syncthreads();
+    if (!flag[0]) return;
+    __threadfence();
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+      uint32_t ya[MAXNP], yb[MAXNP];
+#pragma unroll
+      for (int i = 0; i < MAXNP; ++i) {
+        if (i < rc.np) {
+          ya[i] = i == PR ? S.buf[k] : __ldcg(rs + (size_t)i * 2 * N + k);
+          yb[i] = i == PR ? S.buf[N + k] : __ldcg(rs + (size_t)i * 2 * N + N + k);
+        }
+      }
+      crt_out(k, ya, yb, body_sum(k));
+    }
+    __syncthreads();
+    // the row's residues are dead: drop their L2 lines without writing them back
+    for (int w = threadIdx.x * 32; w < crt_row_words(rc); w += blockDim.x * 32)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(rs + w) : "memory");
+    return;
   }
+
+  // ---- body term of this CTA's slice, into the (now free) accumulator region while the
+  // other CTAs of the cluster finish ----
+  uint64_t* bsum_s = reinterpret_cast<uint64_t*>(S.acc);  // (k1 - k0) u64 <= N u64
+  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) bsum_s[k - k0] = body_sum(k);
 
   // ---- explicit CRT across the cluster through distributed shared memory (push) ----
   // every CTA stores its residues of each peer's slice into that peer's (dead) mask
@@ -694,22 +750,15 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   const uint32_t* recv = reinterpret_cast<const uint32_t*>(S.xa);
   for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-    uint64_t ua = 0, ub = 0;
-    double fa = 0.0, fb = 0.0;
+    uint32_t ya[MAXNP], yb[MAXNP];
 #pragma unroll
     for (int i = 0; i < MAXNP; ++i) {
       if (i < rc.np) {
-        const uint32_t ya = recv[(size_t)i * 2 * per + (k - k0)], yb = recv[(size_t)i * 2 * per + per + (k - k0)];
-        ua += (uint64_t)ya * rc.pc[i].q_mod64;
-        ub += (uint64_t)yb * rc.pc[i].q_mod64;
-        fa += (double)ya * rc.pc[i].inv_p;
-        fb += (double)yb * rc.pc[i].inv_p;
+        ya[i] = recv[(size_t)i * 2 * per + (k - k0)];
+        yb[i] = recv[(size_t)i * 2 * per + per + (k - k0)];
       }
     }
-    const uint64_t Av = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
-    const uint64_t Bv = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
-    xout[k] = ((a.identity ? xin[k] : 0ull) - Av) & QMASK;
-    xout[N + k] = (bsum_s[k - k0] - Bv) & QMASK;
+    crt_out(k, ya, yb, bsum_s[k - k0]);
   }
 }
 
@@ -757,7 +806,7 @@ template <int T, int A, int L>
 __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMinBlocks)
     ks_stage_kernel(const __grid_constant__ RingConst rc, const __grid_constant__ StageArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const unsigned rank = cg::this_cluster().block_rank();
+  const unsigned rank = a.independent ? blockIdx.x % rc.np : cg::this_cluster().block_rank();
   switch (rank) {
     case 0: stage_body<T, A, L, 0>(rc, a, smem); break;
     case 1: stage_body<T, A, L, 1>(rc, a, smem); break;
@@ -857,7 +906,7 @@ static cudaError_t launch_stage_tal(const RingConst& rc, const StageArgs& a, cud
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = a.independent ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, rc, a);
 }
 

@@ -31,7 +31,18 @@ struct StageArgs {
   // nsplit then sums the partials (0 or 1: one set)
   uint32_t* acc_out;
   int nsplit;
+  // independent CTAs (no cluster launch; the CTA's prime is blockIdx % np): set for acc_out
+  // launches (no CRT) and for the L2 CRT: each CTA stores its residues of the row in
+  // crt_scratch [B][crt_row_words] and the last of the row's CTAs (crt_cnt [B], zeroed by the
+  // host) combines them
+  int independent;
+  uint32_t* crt_scratch;
+  unsigned* crt_cnt;
 };
+// u32 words of one row's CRT residues in the L2 CRT scratch (np x 2 x N, 128-byte lines)
+inline __host__ __device__ size_t crt_row_words(const RingConst& rc) {
+  return ((size_t)rc.np * 2 * rc.N + 31) & ~(size_t)31;
+}
 
 struct SpecArgs {
   const uint64_t* keys;   // (jobs, N) key polynomials, job = (slot*l + i)*2 + c
