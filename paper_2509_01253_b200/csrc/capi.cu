@@ -194,8 +194,9 @@ int64_t crt_min_rows() {
 }
 
 // launch a stage (or the acc_in tail of a split / tensor-core stage) with the configured CRT;
-// rows go in chunks so that the CRT scratch stays a few hundred MB
-constexpr int64_t CRT_CHUNK_ROWS = 8192;
+// rows go in equal chunks of at most CRT_CHUNK_ROWS (scratch <= 1.6 GB at b = 12; its lines are
+// discarded from L2 after use, so it costs address space, not HBM traffic)
+constexpr int64_t CRT_CHUNK_ROWS = 32768;
 int launch_stage_crt(sfhr_ctx* ctx, const StageArgs& a, cudaStream_t st, const char* what) {
   const RingConst& rc = ctx->plan.rc;
   if (stage_clusters() || a.B < crt_min_rows()) {
@@ -203,7 +204,8 @@ int launch_stage_crt(sfhr_ctx* ctx, const StageArgs& a, cudaStream_t st, const c
     return SFHR_OK;
   }
   const size_t row_words = crt_row_words(rc);
-  const int64_t chunk = std::min<int64_t>(a.B, CRT_CHUNK_ROWS);
+  const int64_t nch = (a.B + CRT_CHUNK_ROWS - 1) / CRT_CHUNK_ROWS;
+  const int64_t chunk = (a.B + nch - 1) / nch;
   const size_t scratch_bytes = (size_t)chunk * row_words * 4;
   uint32_t* ws = nullptr;
   if (const int rc_ = grow_workspace(ctx->crt_ws, ctx->crt_ws_bytes, ctx->crt_ws_free,

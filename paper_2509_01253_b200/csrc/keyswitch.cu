@@ -700,13 +700,17 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       const uint4* src = reinterpret_cast<const uint4*>(S.buf);
       for (int c = threadIdx.x; c < N / 2; c += blockDim.x) mine[c] = src[c];  // 2N u32
     }
-    __threadfence();
+    // release: the barrier orders the CTA's stores before thread 0's gpu-scope fence (cumulative)
     __syncthreads();
     uint32_t* flag = reinterpret_cast<uint32_t*>(S.acc);  // free after the inverse transforms
-    if (threadIdx.x == 0) flag[0] = atomicAdd(a.crt_cnt + row, 1u) == (unsigned)(rc.np - 1);
+    if (threadIdx.x == 0) {
+      // acq_rel: releases this CTA's residues and, for the last arriver, acquires the peers'
+      unsigned old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.crt_cnt + row) : "memory");
+      flag[0] = old == (unsigned)(rc.np - 1);
+    }
     __syncthreads();
     if (!flag[0]) return;
-    __threadfence();
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
       uint32_t ya[MAXNP], yb[MAXNP];
 #pragma unroll
