@@ -179,6 +179,16 @@ bool stage_clusters() {
   return on;
 }
 
+// items per prime-major CTA group of an independent stage launch (SFHR_STAGE_GROUP; default
+// 444 = one wave of b = 12 CTAs on 148 SMs)
+int stage_group() {
+  static const int v = [] {
+    const char* e = std::getenv("SFHR_STAGE_GROUP");
+    return e ? std::atoi(e) : 444;
+  }();
+  return v;
+}
+
 // launches with fewer rows than this keep the cluster CRT: they are latency bound, and the L2
 // CRT's last arriver serialises the whole row's CRT (SFHR_CRT_MIN_ROWS, default one row per SM)
 int64_t crt_min_rows() {
@@ -222,6 +232,7 @@ int launch_stage_crt(sfhr_ctx* ctx, const StageArgs& a, cudaStream_t st, const c
     c.independent = 1;
     c.crt_scratch = ws;
     c.crt_cnt = cnt;
+    c.group = stage_group();
     CK(cudaMemsetAsync(cnt, 0, (size_t)c.B * 4, st), "CRT counters");
     CK(launch_stage(rc, c, st), what);
     if (r0) ++g_launches;  // the callers count one launch per stage
@@ -375,6 +386,7 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     s1.acc_out = ws;
     s1.nsplit = split;
     s1.independent = 1;  // no CRT in this half: its CTAs never talk to each other
+    s1.group = stage_group();
     CK(launch_stage(P.rc, s1, st), "stage kernel (representative split)");
     StageArgs s2 = a;
     s2.acc_in = ws;

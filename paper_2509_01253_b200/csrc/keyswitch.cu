@@ -775,13 +775,12 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 
 // a cluster processes SFHR_ROWS_PER_CLUSTER consecutive rows (twiddles staged once)
 template <int T, int A, int L, int PR>
-__device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem) {
-  if (a.acc_out && a.nsplit > 1) {  // representative split: cluster = (row, split)
-    const int64_t cid = blockIdx.x / rc.np;
-    stage_row<T, A, L, PR>(rc, a, smem, cid / a.nsplit, true, (int)(cid % a.nsplit));
+__device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem, const int64_t item) {
+  if (a.acc_out && a.nsplit > 1) {  // representative split: item = (row, split)
+    stage_row<T, A, L, PR>(rc, a, smem, item / a.nsplit, true, (int)(item % a.nsplit));
     return;
   }
-  const int64_t row0 = (int64_t)(blockIdx.x / rc.np) * SFHR_ROWS_PER_CLUSTER;
+  const int64_t row0 = item * SFHR_ROWS_PER_CLUSTER;
   for (int rr = 0; rr < SFHR_ROWS_PER_CLUSTER; ++rr) {
     if (row0 + rr >= a.B) break;  // uniform across the cluster
     stage_row<T, A, L, PR>(rc, a, smem, row0 + rr, rr == 0);
@@ -810,12 +809,29 @@ template <int T, int A, int L>
 __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMinBlocks)
     ks_stage_kernel(const __grid_constant__ RingConst rc, const __grid_constant__ StageArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const unsigned rank = a.independent ? blockIdx.x % rc.np : cg::this_cluster().block_rank();
+  // item = row (or (row, split) of a representative-split launch) and the CTA's CRT prime
+  int64_t item = blockIdx.x / rc.np;
+  unsigned rank;
+  if (!a.independent) {
+    rank = cg::this_cluster().block_rank();
+  } else if (a.group > 0) {
+    // prime-major groups of `group` items: the CTAs resident at any time run one or two of the
+    // np prime specialisations of this kernel, not all of them (instruction-cache footprint)
+    const int64_t nitems = a.acc_out && a.nsplit > 1 ? a.B * a.nsplit : a.B;
+    const int64_t per_group = (int64_t)a.group * rc.np;
+    const int64_t g = blockIdx.x / per_group, base = g * a.group;
+    const int64_t gc = nitems - base < a.group ? nitems - base : a.group;
+    const int64_t within = blockIdx.x - g * per_group;
+    rank = (unsigned)(within / gc);
+    item = base + within % gc;
+  } else {
+    rank = blockIdx.x % rc.np;
+  }
   switch (rank) {
-    case 0: stage_body<T, A, L, 0>(rc, a, smem); break;
-    case 1: stage_body<T, A, L, 1>(rc, a, smem); break;
-    case 2: stage_body<T, A, L, 2>(rc, a, smem); break;
-    default: stage_body<T, A, L, 3>(rc, a, smem); break;
+    case 0: stage_body<T, A, L, 0>(rc, a, smem, item); break;
+    case 1: stage_body<T, A, L, 1>(rc, a, smem, item); break;
+    case 2: stage_body<T, A, L, 2>(rc, a, smem, item); break;
+    default: stage_body<T, A, L, 3>(rc, a, smem, item); break;
   }
 }
 

@@ -38,6 +38,7 @@ struct StageArgs {
   int independent;
   uint32_t* crt_scratch;
   unsigned* crt_cnt;
+  int group;  // independent CTAs: items per prime-major group (0: prime = blockIdx % np)
 };
 // u32 words of one row's CRT residues in the L2 CRT scratch (np x 2 x N, 128-byte lines)
 inline __host__ __device__ size_t crt_row_words(const RingConst& rc) {
