@@ -232,7 +232,9 @@ int launch_stage_crt(sfhr_ctx* ctx, const StageArgs& a, cudaStream_t st, const c
     c.independent = 1;
     c.crt_scratch = ws;
     c.crt_cnt = cnt;
-    c.group = stage_group();
+    // prime-major groups only for launches of several waves: in a short launch they push every
+    // row's last arriver (the CRT) to the end of the launch
+    c.group = c.B >= 4 * (int64_t)stage_group() ? stage_group() : 0;
     CK(cudaMemsetAsync(cnt, 0, (size_t)c.B * 4, st), "CRT counters");
     CK(launch_stage(rc, c, st), what);
     if (r0) ++g_launches;  // the callers count one launch per stage
@@ -386,7 +388,7 @@ int run_stage(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nrep
     s1.acc_out = ws;
     s1.nsplit = split;
     s1.independent = 1;  // no CRT in this half: its CTAs never talk to each other
-    s1.group = stage_group();
+    s1.group = B * split >= 4 * (int64_t)stage_group() ? stage_group() : 0;
     CK(launch_stage(P.rc, s1, st), "stage kernel (representative split)");
     StageArgs s2 = a;
     s2.acc_in = ws;
