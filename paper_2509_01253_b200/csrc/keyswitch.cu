@@ -128,6 +128,15 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
 #ifndef SFHR_WINO7_INV1
 #define SFHR_WINO7_INV1 1
 #endif
+// lazy ranges (A/B knobs): inverse DFT outputs that feed a twiddle multiply stay unreduced
+// (the next stage Barrett-reduces only its x_0); the last forward stage feeds the key MAC
+// unreduced when l >= 3 (one REDC + Barrett per accumulator instead of one Barrett per digit)
+#ifndef SFHR_LAZY_INV
+#define SFHR_LAZY_INV 1
+#endif
+#ifndef SFHR_LAZY_MAC
+#define SFHR_LAZY_MAC 1
+#endif
 
 // Rader/Winograd radix-7 DFT (constants and range proof: plan.cpp build_wino7).  The integer
 // multiply (fmaheavy) pipe bounds the stage kernel, so products are what to save: 10 IMAD.WIDE
@@ -252,6 +261,21 @@ __device__ __forceinline__ void dft_inv_red(const uint32_t (&x)[T], uint32_t (&y
   else if (SFHR_SYM_DFT) dft_sym<T, true, true>(x, y, pc);
   else dft_t<T>(x, y, pc.zi, pc.p, pc.pinv);
 }
+// inverse DFT whose k >= 1 outputs are only ever multiplied by a twiddle next (y_0 in [0, 2p),
+// y_k < 2^32): every consumer either Montgomery-multiplies an input (any a < 2^32 keeps
+// a * bm < p 2^32) or Barrett-reduces it first (the x_0 of the next inverse stage)
+template <int T>
+__device__ __forceinline__ void dft_inv_lazy(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
+  if constexpr (T == 7 && SFHR_WINO7) dft_wino7<true, false>(x, y, pc);
+  else if constexpr (T == 5 && SFHR_WINO5) dft_wino5<true, false>(x, y, pc);
+  else if (SFHR_SYM_DFT) dft_sym<T, true, false>(x, y, pc);
+  else dft_t<T>(x, y, pc.zi, pc.p, pc.pinv);
+}
+template <int T>
+__device__ __forceinline__ void dft_inv(const uint32_t (&x)[T], uint32_t (&y)[T], const PrimeConst& pc) {
+  if (SFHR_LAZY_INV) dft_inv_lazy<T>(x, y, pc);
+  else dft_inv_red<T>(x, y, pc);
+}
 
 __device__ __forceinline__ uint32_t lift_signed(int d, uint32_t p) {
   return d < 0 ? (uint32_t)(d + (int)p) : (uint32_t)d;
@@ -282,6 +306,10 @@ __device__ __forceinline__ void fwd_first_step(uint32_t* buf, int nb, const Ring
   }
   __syncthreads();
 }
+
+// lazy MAC pays off from three digits on (one Barrett per accumulator vs one per digit)
+template <int L>
+constexpr bool kLazyMac = SFHR_LAZY_MAC && L >= 3;
 
 // mid-stage work order: item-major (one item's index math for all digit buffers) for t <= 5
 template <int T>
@@ -344,10 +372,11 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
     const int step = g.M / (T * L);
     auto item = [&](uint32_t* v, int e1) {
       uint32_t z[T], x[T];
-      z[0] = v[0];
+      // lazy: v[0] is some earlier stage's unreduced output (< 2^32)
+      z[0] = SFHR_LAZY_INV ? v[0] - __umulhi(v[0], pc.mu) * pc.p : v[0];
 #pragma unroll
       for (int k = 1; k < T; ++k) z[k] = mont_mul(v[k * L], wt[g.M - e1 * k], pc.p, pc.pinv);
-      dft_inv_red<T>(z, x, pc);
+      dft_inv<T>(z, x, pc);
 #pragma unroll
       for (int m = 0; m < T; ++m) v[m * L] = x[m];
     };
@@ -586,7 +615,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
         uint32_t x[T], yv[T];
 #pragma unroll
         for (int m = 0; m < T; ++m) x[m] = v[m];
-        dft_fwd_red<T>(x, yv, pc);
+        if constexpr (kLazyMac<L>) dft_fwd_tw<T>(x, yv, pc);  // y_k < 2^32
+        else dft_fwd_red<T>(x, yv, pc);
         const uint32_t* ka = ks + ((size_t)(i * 2 + 0) * rc.np + PR) * N + item;
         const uint32_t* kb = ks + ((size_t)(i * 2 + 1) * rc.np + PR) * N + item;
 #pragma unroll
@@ -595,12 +625,18 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
           tb[k] += (uint64_t)yv[k] * __ldg(kb + k * g.nitems);
         }
       }
-      // L products of (<2p)(<p) < p 2^32 (p < 2^31/L): one REDC each; sum over reps < 2 reps p
+      // L products of (<2p)(<p) < p 2^32 (p < 2^31/L): one REDC each; sum over reps < 2 reps p.
+      // Lazy MAC: L products of (<2^32)(<p) < L p 2^32 (< 2^64): the REDC lands in (0, (L+1) p)
+      // (< 2^32), one Barrett step brings it to [0, 2p)
       uint32_t* aa = S.acc + item * T;
       uint32_t* ab = S.acc + N + item * T;
 #pragma unroll
       for (int k = 0; k < T; ++k) {
-        const uint32_t ra = redc(ta[k], p, pinv), rb2 = redc(tb[k], p, pinv);
+        uint32_t ra = redc(ta[k], p, pinv), rb2 = redc(tb[k], p, pinv);
+        if constexpr (kLazyMac<L>) {
+          ra -= __umulhi(ra, mu) * p;
+          rb2 -= __umulhi(rb2, mu) * p;
+        }
         aa[k] = r > rb ? aa[k] + ra : ra;
         ab[k] = r > rb ? ab[k] + rb2 : rb2;
       }
@@ -625,8 +661,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       za[k] = va - __umulhi(va, mu) * p;  // -> [0, 2p)
       zb[k] = vb - __umulhi(vb, mu) * p;
     }
-    dft_inv_red<T>(za, xa, pc);
-    dft_inv_red<T>(zb, xb, pc);
+    dft_inv<T>(za, xa, pc);
+    dft_inv<T>(zb, xb, pc);
 #pragma unroll
     for (int m = 0; m < T; ++m) {
       S.buf[item * T + m] = xa[m];

@@ -84,6 +84,16 @@ class Prime:
         assert np.all(r < U(2) * self.p)
         return r
 
+    def redc_lazy(self, x, l):
+        """REDC of a lazy key-MAC sum (< l p 2^32), then one Barrett step -> [0, 2p)."""
+        x = np.asarray(x, dtype=U)
+        hi = x >> U(32)
+        assert np.all(hi < U(l) * self.p), "lazy MAC sum >= l p 2^32"
+        m = ((x & M32) * self.pinv) & M32
+        r = hi + self.p - ((m * self.p) >> U(32))
+        assert np.all(r < U(1 << 32))
+        return self.barrett(r)
+
     def mont(self, a, bm):
         a = np.asarray(a, dtype=U)
         assert np.all(a < U(2) * self.p)
@@ -258,8 +268,13 @@ class Prime:
         return self.redc(a * np.asarray(bm, dtype=U))
 
 
-def forward(sp: SimPlan, pr: Prime, vals):
-    """vals: (N,) residues < 2p (coefficient domain) -> (nitems, T) last-stage outputs."""
+LAZY_INV = True   # keyswitch.cu SFHR_LAZY_INV
+LAZY_MAC = True   # keyswitch.cu SFHR_LAZY_MAC (applies from l >= 3)
+
+
+def forward(sp: SimPlan, pr: Prime, vals, red=True):
+    """vals: (N,) residues < 2p (coefficient domain) -> (nitems, T) last-stage outputs
+    (in [0, 2p) when red, else the lazy last stage: < 2^32)."""
     T, n1, M = sp.t, sp.n1, sp.M
     A = np.asarray(vals, dtype=U).reshape(T - 1, n1)
     m = np.arange(n1)
@@ -284,29 +299,31 @@ def forward(sp: SimPlan, pr: Prime, vals):
         buf = nv.reshape(-1)
         L //= T
     x = buf.reshape(sp.nitems, T)
-    ys = pr.dft_k([x[:, mm] for mm in range(T)], red=True)
+    ys = pr.dft_k([x[:, mm] for mm in range(T)], red=red)
     return np.stack(ys, axis=1)  # (nitems, T)
 
 
 def inverse(sp: SimPlan, pr: Prime, y):
     """y: (nitems, T) in [0,2p) -> (N,) CRT-weighted residues y_i in [0, p)."""
     T, n1, M = sp.t, sp.n1, sp.M
-    xs = pr.dft_k([y[:, k] for k in range(T)], inv=True, red=True)
+    lazy = LAZY_INV
+    xs = pr.dft_k([y[:, k] for k in range(T)], inv=True, red=not lazy)
     buf = np.stack(xs, axis=1).reshape(-1)
     L = T
+    mul = pr.mont6 if lazy else pr.mont   # twiddle multiply of a lazy (< 2^32) operand
     for s_ in range(sp.alpha - 3, -1, -1):
         blocks = T ** s_
         v = buf.reshape(T - 1, blocks, T, L)
         step = M // (T * L)
         j = np.arange(L)
-        zs = [v[:, :, 0, :]] + [pr.mont(v[:, :, k, :], pr.wt[M - step * j * k][None, None, :])
-                               for k in range(1, T)]
-        xs = pr.dft_k(zs, inv=True, red=True)
+        z0 = pr.barrett(v[:, :, 0, :]) if lazy else v[:, :, 0, :]
+        zs = [z0] + [mul(v[:, :, k, :], pr.wt[M - step * j * k][None, None, :]) for k in range(1, T)]
+        xs = pr.dft_k(zs, inv=True, red=not lazy)
         buf = np.stack(xs, axis=2).reshape(-1)
         L *= T
     v = buf.reshape(T - 1, n1)
     m = np.arange(n1)
-    Cs = [pr.mont(v[r - 1], pr.wt[M - r * m]) for r in range(1, T)]
+    Cs = [mul(v[r - 1], pr.wt[M - r * m]) for r in range(1, T)]
     if T == 7:
         return pr.inv_first7(Cs).reshape(-1)
     out = np.zeros((T - 1, n1), U)
@@ -343,13 +360,20 @@ def stage_row(sp: SimPlan, x, reps_dinv_keys, identity, decompose, automorph_u64
             digs = decompose(y)
             ta = np.zeros((sp.nitems, sp.t), U)
             tb = np.zeros((sp.nitems, sp.t), U)
+            lazy = LAZY_MAC and sp.l >= 3
             for li in range(sp.l):
                 dm = np.where(digs[li] < 0, digs[li] + int(pr.p), digs[li]).astype(U)
-                out = forward(sp, pr, dm)
+                out = forward(sp, pr, dm, red=not lazy)
+                pa, pb = ta, tb
                 ta = ta + out * key_spectrum(sp, pr, keys[li][0])
                 tb = tb + out * key_spectrum(sp, pr, keys[li][1])
-            accA = accA + pr.redc(ta)   # one REDC per rep into a u32 accumulator
-            accB = accB + pr.redc(tb)
+                assert np.all(ta >= pa) and np.all(tb >= pb), "MAC accumulator wrapped"
+            if lazy:   # REDC of a sum < l p 2^32 lands in (0, (l + 1) p); one Barrett step
+                ra, rb = pr.redc_lazy(ta, sp.l), pr.redc_lazy(tb, sp.l)
+            else:      # one REDC per rep into a u32 accumulator
+                ra, rb = pr.redc(ta), pr.redc(tb)
+            accA = accA + ra
+            accB = accB + rb
             assert np.all(accA < U(1 << 32)) and np.all(accB < U(1 << 32))
         barrett = lambda v: v - ((v * pr.mu) >> U(32)) * pr.p  # noqa: E731
         za, zb = barrett(accA), barrett(accB)
