@@ -315,10 +315,15 @@ constexpr bool kLazyMac = SFHR_LAZY_MAC && L >= 3;
 template <int T>
 constexpr bool kItemMajor = T <= 5;
 
-// forward DIF stages s = 0 .. alpha-3 (all but the last, span > 1)
-template <int T, int A, int PR>
+#ifndef SFHR_SHOUP_MID
+#define SFHR_SHOUP_MID 1
+#endif
+
+// forward DIF stages s = 0 .. alpha-3 (all but the last, span > 1).  SH: twiddles from the Shoup
+// pairs sh[e / t] (every mid-stage exponent is a multiple of t) instead of the Montgomery table
+template <int T, int A, int PR, bool SH = false>
 __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const RingConst& rc,
-                                               const uint32_t* wt) {
+                                               const uint32_t* wt, const uint2* sh = nullptr) {
   const PrimeConst& pc = rc.pc[PR];
   const Geo<T, A> g(rc);
   const int nsub = g.n1 / T;
@@ -327,14 +332,22 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
     if (!A && s >= g.alpha - 2) break;
     const int L = A ? cpow(T, A - 2 - s) : nsub / cpow(T, s);
     const int step = g.M / (T * L);
-    auto item = [&](uint32_t* v, int e1) {
+    const int stepT = step / T;  // exact: L <= n1 / T
+    auto item = [&](uint32_t* v, const int j) {
+      const int e1 = step * j;
       uint32_t x[T], y[T];
 #pragma unroll
       for (int m = 0; m < T; ++m) x[m] = v[m * L];
       dft_fwd_tw<T>(x, y, pc);
       v[0] = y[0];
+      if constexpr (SH) {
+        const int es = stepT * j;  // e1 / t
 #pragma unroll
-      for (int k = 1; k < T; ++k) v[k * L] = mont_mul(y[k], wt[e1 * k], pc.p, pc.pinv);
+        for (int k = 1; k < T; ++k) v[k * L] = shoup_mul(y[k], sh[es * k], pc.p);
+      } else {
+#pragma unroll
+        for (int k = 1; k < T; ++k) v[k * L] = mont_mul(y[k], wt[e1 * k], pc.p, pc.pinv);
+      }
     };
     if constexpr (kItemMajor<T>) {
       // item-major, buffers inner: position and twiddle exponent computed once for all nb
@@ -344,14 +357,16 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
         const int b = rem / L, j = rem - b * L;
         const int off = sub * g.n1 + b * T * L + j;
 #pragma unroll 1
-        for (int q = 0; q < nb; ++q) item(buf + q * g.N + off, step * j);
+        for (int q = 0; q < nb; ++q) item(buf + q * g.N + off, j);
       }
     } else {
+      // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
+      // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
+      // (two constant divisions instead of three; none at the first stage, where L = nsub)
       for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
-        const int q = w / g.nitems, it = w - q * g.nitems;
-        const int sub = it / nsub, rem = it - sub * nsub;
-        const int b = rem / L, j = rem - b * L;
-        item(buf + q * g.N + sub * g.n1 + b * T * L + j, step * j);
+        const int P = w / nsub, r = w - P * nsub;
+        const int b = L == nsub ? 0 : r / L, j = r - b * L;
+        item(buf + P * g.n1 + r + b * (T - 1) * L, j);
       }
     }
     __syncthreads();
@@ -359,9 +374,9 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
 }
 
 // inverse DIT stages s = alpha-3 .. 0 (the span-1 stage is undone in registers)
-template <int T, int A, int PR>
+template <int T, int A, int PR, bool SH = false>
 __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const RingConst& rc,
-                                               const uint32_t* wt) {
+                                               const uint32_t* wt, const uint2* sh = nullptr) {
   const PrimeConst& pc = rc.pc[PR];
   const Geo<T, A> g(rc);
   const int nsub = g.n1 / T;
@@ -370,12 +385,20 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
     if (!A && si >= g.alpha - 2) break;
     const int L = cpow(T, si + 1);
     const int step = g.M / (T * L);
-    auto item = [&](uint32_t* v, int e1) {
+    const int stepT = step / T;
+    auto item = [&](uint32_t* v, const int j) {
+      const int e1 = step * j;
       uint32_t z[T], x[T];
       // lazy: v[0] is some earlier stage's unreduced output (< 2^32)
       z[0] = SFHR_LAZY_INV ? v[0] - __umulhi(v[0], pc.mu) * pc.p : v[0];
+      if constexpr (SH) {
+        const int es = stepT * j;  // omega^(M - e1 k) = sh[n1 - es k]
 #pragma unroll
-      for (int k = 1; k < T; ++k) z[k] = mont_mul(v[k * L], wt[g.M - e1 * k], pc.p, pc.pinv);
+        for (int k = 1; k < T; ++k) z[k] = shoup_mul(v[k * L], sh[g.n1 - es * k], pc.p);
+      } else {
+#pragma unroll
+        for (int k = 1; k < T; ++k) z[k] = mont_mul(v[k * L], wt[g.M - e1 * k], pc.p, pc.pinv);
+      }
       dft_inv<T>(z, x, pc);
 #pragma unroll
       for (int m = 0; m < T; ++m) v[m * L] = x[m];
@@ -386,14 +409,16 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
         const int b = rem / L, j = rem - b * L;
         const int off = sub * g.n1 + b * T * L + j;
 #pragma unroll 1
-        for (int q = 0; q < nb; ++q) item(buf + q * g.N + off, step * j);
+        for (int q = 0; q < nb; ++q) item(buf + q * g.N + off, j);
       }
     } else {
+      // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
+      // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
+      // (two constant divisions instead of three; none at the first stage, where L = nsub)
       for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
-        const int q = w / g.nitems, it = w - q * g.nitems;
-        const int sub = it / nsub, rem = it - sub * nsub;
-        const int b = rem / L, j = rem - b * L;
-        item(buf + q * g.N + sub * g.n1 + b * T * L + j, step * j);
+        const int P = w / nsub, r = w - P * nsub;
+        const int b = L == nsub ? 0 : r / L, j = r - b * L;
+        item(buf + P * g.n1 + r + b * (T - 1) * L, j);
       }
     }
     __syncthreads();
@@ -436,22 +461,25 @@ __device__ __forceinline__ void inv_first_step(uint32_t* buf, int nb, const Ring
 struct SmemLayout {
   uint64_t* xa;   // (N,) staged mask component of the row
   uint32_t* wt;   // (M+1,) Montgomery twiddles of this CTA's prime
+  uint2* sh;      // (n1+1,) Shoup pairs of the exponents t i (mid-stage twiddles)
   uint32_t* acc;  // (2, N) NTT-domain accumulators, summed over reps
   uint32_t* buf;  // (nb, N) transform buffers
 };
 
 // the mask buffer doubles as the CRT receive buffer [np][2][per] u32 (per = ceil(N / np))
+// (32-bit arithmetic: a 64-bit division by the runtime np cost ~2 % of the kernel's instructions)
 __host__ __device__ __forceinline__ size_t xa_region_bytes(const RingConst& rc) {
-  const size_t per = (size_t)(rc.N + rc.np - 1) / rc.np;
-  const size_t recv = (size_t)rc.np * 2 * per * 4, mask = (size_t)rc.N * 8;
-  return ((recv > mask ? recv : mask) + 15) & ~(size_t)15;
+  const unsigned per = ((unsigned)rc.N + (unsigned)rc.np - 1u) / (unsigned)rc.np;
+  const unsigned recv = (unsigned)rc.np * 2u * per * 4u, mask = (unsigned)rc.N * 8u;
+  return (size_t)(((recv > mask ? recv : mask) + 15u) & ~15u);
 }
 
 __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst& rc) {
   SmemLayout s;
   s.xa = reinterpret_cast<uint64_t*>(smem);
   s.wt = reinterpret_cast<uint32_t*>(smem + xa_region_bytes(rc));
-  s.acc = s.wt + twid_stride(rc.M);
+  s.sh = reinterpret_cast<uint2*>(s.wt + twid_stride(rc.M));
+  s.acc = s.wt + twid_stride(rc.M) + shoup_stride(rc.n1);
   s.buf = s.acc + 2 * rc.N;
   return s;
 }
@@ -484,6 +512,12 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     const uint4* wsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)PR * twid_stride(M));
     uint4* wdst = reinterpret_cast<uint4*>(S.wt);
     for (int k = threadIdx.x; k < twid_stride(M) / 4; k += blockDim.x) wdst[k] = wsrc[k];
+    if (SFHR_SHOUP_MID) {
+      const uint4* hsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)rc.np * twid_stride(M) +
+                                                         (size_t)PR * shoup_stride(n1));
+      uint4* hdst = reinterpret_cast<uint4*>(S.sh);
+      for (int k = threadIdx.x; k < shoup_stride(n1) / 4; k += blockDim.x) hdst[k] = hsrc[k];
+    }
   }
   int live = __syncthreads_or(nz);
   if (!live) {
@@ -599,7 +633,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     // ---- B: first step + mid stages of the l digit transforms ----
     fwd_first_step<T, A, PR>(S.buf, L, rc, S.wt);
 #endif
-    fwd_mid_stages<T, A, PR>(S.buf, L, rc, S.wt);
+    fwd_mid_stages<T, A, PR, SFHR_SHOUP_MID>(S.buf, L, rc, S.wt, S.sh);
     // the staged mask is dead after the last rep's gathers: tell the peers they may push
     // their CRT residues into it (the matching wait precedes our own pushes)
     if (r == a.nreps - 1 && !a.independent) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
@@ -670,7 +704,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
   }
   __syncthreads();
-  inv_mid_stages<T, A, PR>(S.buf, 2, rc, S.wt);
+  inv_mid_stages<T, A, PR, SFHR_SHOUP_MID>(S.buf, 2, rc, S.wt, S.sh);
   inv_first_step<T, A, PR>(S.buf, 2, rc, S.wt);
 
   // body term x.b + sum_r aut_r(x.b) of coefficient k, gathered from global
@@ -813,7 +847,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 template <int T, int A, int L, int PR>
 __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem, const int64_t item) {
   if (a.acc_out && a.nsplit > 1) {  // representative split: item = (row, split)
-    stage_row<T, A, L, PR>(rc, a, smem, item / a.nsplit, true, (int)(item % a.nsplit));
+    const unsigned r = (unsigned)item / (unsigned)a.nsplit;
+    stage_row<T, A, L, PR>(rc, a, smem, r, true, (int)((unsigned)item - r * (unsigned)a.nsplit));
     return;
   }
   const int64_t row0 = item * SFHR_ROWS_PER_CLUSTER;
@@ -853,13 +888,14 @@ __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMin
   } else if (a.group > 0) {
     // prime-major groups of `group` items: the CTAs resident at any time run one or two of the
     // np prime specialisations of this kernel, not all of them (instruction-cache footprint)
-    const int64_t nitems = a.acc_out && a.nsplit > 1 ? a.B * a.nsplit : a.B;
-    const int64_t per_group = (int64_t)a.group * rc.np;
-    const int64_t g = blockIdx.x / per_group, base = g * a.group;
-    const int64_t gc = nitems - base < a.group ? nitems - base : a.group;
-    const int64_t within = blockIdx.x - g * per_group;
-    rank = (unsigned)(within / gc);
-    item = base + within % gc;
+    // (32-bit: the grid has < 2^31 CTAs; 64-bit divisions here cost ~1 % of the instructions)
+    const unsigned nitems = (unsigned)(a.acc_out && a.nsplit > 1 ? a.B * a.nsplit : a.B);
+    const unsigned per_group = (unsigned)a.group * (unsigned)rc.np;
+    const unsigned g = blockIdx.x / per_group, base = g * (unsigned)a.group;
+    const unsigned gc = nitems - base < (unsigned)a.group ? nitems - base : (unsigned)a.group;
+    const unsigned within = blockIdx.x - g * per_group;
+    rank = within / gc;
+    item = base + (within - rank * gc);
   } else {
     rank = blockIdx.x % rc.np;
   }
@@ -925,7 +961,8 @@ __global__ void __launch_bounds__(512) ks_spectra_kernel(const __grid_constant__
 #if !defined(SFHR_KS_T)
 size_t stage_smem_bytes(const RingConst& rc) {
   const int nb = rc.l > 2 ? rc.l : 2;
-  return xa_region_bytes(rc) + (size_t)twid_stride(rc.M) * 4 + (size_t)(2 + nb) * rc.N * 4;
+  return xa_region_bytes(rc) + (size_t)(twid_stride(rc.M) + shoup_stride(rc.n1)) * 4 +
+         (size_t)(2 + nb) * rc.N * 4;
 }
 
 int stage_threads(const RingConst& rc) {

@@ -339,7 +339,8 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
   uint64_t Pmod = 1;
   for (uint64_t p : primes) Pmod *= p;
   rc.P_mod64 = Pmod;
-  P.twid.assign((size_t)rc.np * twid_stride(M), 0);
+  // [np][twid_stride(M)] Montgomery powers, then [np][shoup_stride(n1)] Shoup pairs
+  P.twid.assign((size_t)rc.np * (twid_stride(M) + shoup_stride(M / t)), 0);
   const uint64_t R32 = 1ull << 32;
   for (int i = 0; i < rc.np; ++i) {
     const uint64_t p = primes[i];
@@ -403,8 +404,14 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
         pc.g[j][r - 1] = mont(v);
       }
     uint64_t w = 1;
+    uint32_t* sh = P.twid.data() + (size_t)rc.np * twid_stride(M) + (size_t)i * shoup_stride(M / t);
     for (long long e = 0; e <= M; ++e) {
-      P.twid[(size_t)i * twid_stride(M) + e] = mont(e == M ? 1 : w);
+      const uint64_t we = e == M ? 1 : w;
+      P.twid[(size_t)i * twid_stride(M) + e] = mont(we);
+      if (e % t == 0) {
+        sh[2 * (e / t)] = (uint32_t)we;
+        sh[2 * (e / t) + 1] = (uint32_t)((we << 32) / p);
+      }
       w = mulmod(w, omega, p);
     }
   }

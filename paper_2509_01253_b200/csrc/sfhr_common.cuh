@@ -69,6 +69,14 @@ __host__ __device__
 #endif
 inline constexpr int twid_stride(int M) { return (M + 4) & ~3; }
 
+// Shoup twiddle pairs (w, floor(w 2^32 / p)) of the exponents t i, i = 0..n1 (= M / t): every
+// mid-stage twiddle exponent is a multiple of t.  Row stride in u32 words, after the np rows of
+// the Montgomery table in the same allocation
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline constexpr int shoup_stride(int n1) { return (2 * (n1 + 1) + 3) & ~3; }
+
 #ifdef __CUDACC__
 // x < p * 2^32  ->  x * 2^-32 mod p, in (0, 2p)
 __device__ __forceinline__ uint32_t redc(uint64_t x, uint32_t p, uint32_t pinv) {
@@ -88,6 +96,13 @@ __device__ __forceinline__ uint32_t redc_wide(uint64_t x, uint32_t p, uint32_t p
 // a in [0, 2p), bm = b*R mod p  ->  a*b mod p in (0, 2p)
 __device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t bm, uint32_t p, uint32_t pinv) {
   return redc((uint64_t)a * bm, p, pinv);
+}
+
+// Shoup: x < 2^32, wq = (w, floor(w 2^32 / p)), w < p  ->  x w mod p in [0, 2p)
+// (IMAD.HI + 2 IMAD against IMAD.WIDE + IMAD + IMAD.HI for a Montgomery twiddle)
+__device__ __forceinline__ uint32_t shoup_mul(uint32_t x, uint2 wq, uint32_t p) {
+  const uint32_t q = __umulhi(x, wq.y);
+  return x * wq.x - q * p;
 }
 
 // [0, 2p) -> [0, p)

@@ -35,10 +35,13 @@ class SimPlan:
         self.info = list(info[:k])
         np_ = self.info[3]
         stride = (self.M + 4) & ~3  # csrc/sfhr_common.cuh twid_stride
-        tw = np.zeros(np_ * stride, np.uint32)
+        n1 = self.M // t
+        sstride = (2 * (n1 + 1) + 3) & ~3  # shoup_stride
+        tw = np.zeros(np_ * (stride + sstride), np.uint32)
         nat.check(nat.lib.sfhr_ctx_debug_tables(h, C.byref(rc), C.sizeof(rc), tw.ctypes.data, tw.size))
         self.rc = rc
-        self.tw = tw.reshape(np_, stride)[:, :self.M + 1].astype(U)
+        self.tw = tw[:np_ * stride].reshape(np_, stride)[:, :self.M + 1].astype(U)
+        self.sh = tw[np_ * stride:].reshape(np_, sstride).astype(U)
         self.t, self.alpha, self.N, self.n1 = t, alpha, rc.N, rc.n1
         self.np, self.l = rc.np, rc.l
         self.nitems = rc.nitems
@@ -63,6 +66,13 @@ class Prime:
         self.q_mod64 = U(pc.q_mod64)
         self.inv_p = pc.inv_p
         self.wt = sp.tw[i]
+        self.t = T
+        sh = sp.sh[i]
+        self.sh_w, self.sh_q = sh[0::2][:sp.n1 + 1], sh[1::2][:sp.n1 + 1]
+        # the table is the plain omega^(t i) and floor(w 2^32 / p) (plan.cpp)
+        rinv = pow(1 << 32, -1, int(self.p))
+        assert all(int(self.sh_w[k]) == int(self.wt[T * k]) * rinv % int(self.p) for k in (0, 1, sp.n1))
+        assert all(int(self.sh_q[k]) == (int(self.sh_w[k]) << 32) // int(self.p) for k in (0, 1, sp.n1))
 
     def redc(self, x):
         x = np.asarray(x, dtype=U)
@@ -93,6 +103,18 @@ class Prime:
         r = hi + self.p - ((m * self.p) >> U(32))
         assert np.all(r < U(1 << 32))
         return self.barrett(r)
+
+    def shoup(self, a, e):
+        """shoup_mul (sfhr_common.cuh) by omega^e from the Shoup pair table (e a multiple of t):
+        any a < 2^32 -> [0, 2p)."""
+        a = np.asarray(a, dtype=U)
+        assert np.all(a < U(1 << 32))
+        w = self.sh_w[np.asarray(e) // self.t]
+        wq = self.sh_q[np.asarray(e) // self.t]
+        q = (a * wq) >> U(32)
+        r = (a * w - q * self.p) & M32
+        assert np.all(r < U(2) * self.p), "Shoup product out of [0, 2p)"
+        return r
 
     def mont(self, a, bm):
         a = np.asarray(a, dtype=U)
@@ -270,6 +292,7 @@ class Prime:
 
 LAZY_INV = True   # keyswitch.cu SFHR_LAZY_INV
 LAZY_MAC = True   # keyswitch.cu SFHR_LAZY_MAC (applies from l >= 3)
+SHOUP_MID = True  # keyswitch.cu SFHR_SHOUP_MID (mid-stage twiddles as Shoup products)
 
 
 def forward(sp: SimPlan, pr: Prime, vals, red=True):
@@ -295,7 +318,10 @@ def forward(sp: SimPlan, pr: Prime, vals, red=True):
         nv = np.empty_like(v)
         nv[:, :, 0, :] = ys[0]
         for k in range(1, T):
-            nv[:, :, k, :] = pr.mont6(ys[k], pr.wt[step * j * k][None, None, :])
+            if SHOUP_MID:
+                nv[:, :, k, :] = pr.shoup(ys[k], (step * j * k)[None, None, :])
+            else:
+                nv[:, :, k, :] = pr.mont6(ys[k], pr.wt[step * j * k][None, None, :])
         buf = nv.reshape(-1)
         L //= T
     x = buf.reshape(sp.nitems, T)
@@ -317,7 +343,10 @@ def inverse(sp: SimPlan, pr: Prime, y):
         step = M // (T * L)
         j = np.arange(L)
         z0 = pr.barrett(v[:, :, 0, :]) if lazy else v[:, :, 0, :]
-        zs = [z0] + [mul(v[:, :, k, :], pr.wt[M - step * j * k][None, None, :]) for k in range(1, T)]
+        if SHOUP_MID:
+            zs = [z0] + [pr.shoup(v[:, :, k, :], (M - step * j * k)[None, None, :]) for k in range(1, T)]
+        else:
+            zs = [z0] + [mul(v[:, :, k, :], pr.wt[M - step * j * k][None, None, :]) for k in range(1, T)]
         xs = pr.dft_k(zs, inv=True, red=not lazy)
         buf = np.stack(xs, axis=2).reshape(-1)
         L *= T
