@@ -116,7 +116,8 @@ class LinearDesc(C.Structure):
 class WinoConst(C.Structure):
     _fields_ = [("kT", C.c_uint64), ("kG", C.c_uint64), ("mu", C.c_uint32), ("rho", C.c_int32)] + \
                [(n, C.c_int32) for n in ("a00", "a01", "a10", "b00", "b01", "b10")] + \
-               [(n, C.c_uint32) for n in ("k1p", "k2p", "k3p", "k4p", "k5p", "pad")]
+               [(n, C.c_uint32) for n in ("k1p", "k2p", "k3p", "k4p", "k5p", "mu_w", "mu_q", "rho_w",
+                                          "rho_q", "toff", "pad0", "pad1")]
 
 
 class PrimeConst(C.Structure):

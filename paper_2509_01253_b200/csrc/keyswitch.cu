@@ -128,6 +128,18 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
 #ifndef SFHR_WINO7_INV1
 #define SFHR_WINO7_INV1 1
 #endif
+// the two single-product Rader terms (M0 = S mu, R2 = Tm rho) as Shoup products: IMAD.HI + 2 IMAD
+// against IMAD.WIDE + IMAD + IMAD.HI (plan.cpp bounds both by 2p)
+#ifndef SFHR_WINO_SHOUP
+#define SFHR_WINO_SHOUP 1
+#endif
+__device__ __forceinline__ uint32_t wino_m0(uint32_t S, const WinoConst& w, uint32_t p, uint32_t pinv) {
+  return SFHR_WINO_SHOUP ? shoup_mul(S, make_uint2(w.mu_w, w.mu_q), p) : redc((uint64_t)S * w.mu, p, pinv);
+}
+__device__ __forceinline__ uint32_t wino_r2(int32_t Tm, const WinoConst& w, uint32_t p, uint32_t pinv) {
+  return SFHR_WINO_SHOUP ? shoup_mul((uint32_t)(Tm + (int32_t)w.toff), make_uint2(w.rho_w, w.rho_q), p)
+                         : redc((uint64_t)((int64_t)w.kT + (int64_t)Tm * w.rho), p, pinv);
+}
 // lazy ranges (A/B knobs): inverse DFT outputs that feed a twiddle multiply stay unreduced
 // (the next stage Barrett-reduces only its x_0); the last forward stage feeds the key MAC
 // unreduced when l >= 3 (one REDC + Barrett per accumulator instead of one Barrett per digit)
@@ -154,8 +166,8 @@ __device__ __forceinline__ void dft_wino7(const uint32_t (&x)[7], uint32_t (&y)[
   const int32_t Tm = d03 - d14 + d25;                                               // V(-1)
   const int32_t A0 = (int32_t)(p03 - p25), A1 = (int32_t)(p14 - p25);               // V mod X^2+X+1
   const int32_t C0 = d03 - d25, C1 = d14 + d25;                                     // V mod X^2-X+1
-  const uint32_t M0 = redc((uint64_t)S * w.mu, p, pinv);
-  const uint32_t R2 = redc((uint64_t)((int64_t)w.kT + (int64_t)Tm * w.rho), p, pinv);
+  const uint32_t M0 = wino_m0(S, w, p, pinv);
+  const uint32_t R2 = wino_r2(Tm, w, p, pinv);
   const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
   const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
   const uint32_t h0 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b00 + (int64_t)C1 * w.b01), p, pinv);
@@ -195,8 +207,8 @@ __device__ __forceinline__ void inv_first7(const uint32_t (&C)[6], uint32_t (&o)
   const int32_t Tm = d03 - d14 + d25;
   const int32_t A0 = (int32_t)(p03 - p25), A1 = (int32_t)(p14 - p25);
   const int32_t C0 = d03 - d25, C1 = d14 + d25;
-  const uint32_t S7 = redc((uint64_t)S * w.mu, p, pinv);  // 7 s S / 6
-  const uint32_t R2 = redc((uint64_t)((int64_t)w.kT + (int64_t)Tm * w.rho), p, pinv);
+  const uint32_t S7 = wino_m0(S, w, p, pinv);  // 7 s S / 6
+  const uint32_t R2 = wino_r2(Tm, w, p, pinv);
   const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
   const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
   const uint32_t h0 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b00 + (int64_t)C1 * w.b01), p, pinv);
@@ -222,8 +234,8 @@ __device__ __forceinline__ void dft_wino5(const uint32_t (&x)[5], uint32_t (&y)[
   const uint32_t S = v0 + v1 + v2 + v3;
   const int32_t Tm = (int32_t)(v0 - v1 + v2 - v3);  // V(-1), (-4p, 4p)
   const int32_t A0 = (int32_t)(v0 - v2), A1 = (int32_t)(v1 - v3);  // V mod X^2 + 1
-  const uint32_t M0 = redc((uint64_t)S * w.mu, p, pinv);
-  const uint32_t R2 = redc((uint64_t)((int64_t)w.kT + (int64_t)Tm * w.rho), p, pinv);
+  const uint32_t M0 = wino_m0(S, w, p, pinv);
+  const uint32_t R2 = wino_r2(Tm, w, p, pinv);
   const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
   const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
   const uint32_t X0 = x[0] + M0, Xp = X0 + R2, Xm = X0 - R2;

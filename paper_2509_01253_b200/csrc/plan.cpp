@@ -79,6 +79,12 @@ static int64_t inv_mod_any(int64_t a, int64_t m) {  // gcd(a, m) = 1
   return ((x % m) + m) % m;
 }
 
+// Shoup form (plain constant, floor(c 2^32 / p)) of c in [0, p)
+static void shoup_pair(uint64_t c, uint64_t p, uint32_t& w, uint32_t& q) {
+  w = (uint32_t)(c % p);
+  q = (uint32_t)(((uint64_t)w << 32) / p);
+}
+
 // Tr(zeta_M^k) over Q (reference dual.py:18-27)
 static long long tr_zeta(long long k, int t, int alpha) {
   long long M = 1, n1 = 1;
@@ -121,6 +127,9 @@ static Wino7Bounds wino7_consts(WinoConst& k, uint64_t z, uint64_t scale, uint64
   std::memset(&k, 0, sizeof(k));
   k.mu = (uint32_t)mulmod(mulmod(W1, i6, p), Rm, p);
   k.rho = cen(mulmod(Wm, i6, p));
+  shoup_pair(mulmod(W1, i6, p), p, k.mu_w, k.mu_q);
+  shoup_pair(mulmod(Wm, i6, p), p, k.rho_w, k.rho_q);
+  k.toff = (uint32_t)(6 * p);  // Tm in (-3X, 3X) = (-6p, 6p)
   k.a00 = cen(mulmod(sub(2 * B0 % p, B1), i6, p));
   k.a01 = cen(mulmod(sub(0, (B0 + B1) % p), i6, p));
   k.a10 = cen(mulmod(sub(2 * B1 % p, B0), i6, p));
@@ -131,9 +140,11 @@ static Wino7Bounds wino7_consts(WinoConst& k, uint64_t z, uint64_t scale, uint64
   auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
   k.kT = up(Tmax * ch);
   k.kG = up(2.0L * Amax * ch);
-  if (X + Smax >= two32) throw std::invalid_argument("NTT prime too large for the radix-7 DFT ranges");
-  return {std::floor(Smax * (p - 1) / two32) + p, std::floor(((long double)k.kT + Tmax * ch) / two32) + p,
-          std::floor(((long double)k.kG + 2.0L * Amax * ch) / two32) + p};
+  if (X + Smax >= two32 || 2.0L * Tmax >= two32)
+    throw std::invalid_argument("NTT prime too large for the radix-7 DFT ranges");
+  // M0 and R2 may come from the Shoup forms (keyswitch.cu SFHR_WINO_SHOUP): bound them by 2p
+  const long double M0 = std::floor(Smax * (p - 1) / two32) + p, R2 = std::floor(((long double)k.kT + Tmax * ch) / two32) + p;
+  return {std::max(M0, X), std::max(R2, X), std::floor(((long double)k.kG + 2.0L * Amax * ch) / two32) + p};
 }
 
 static uint32_t up_p(long double v, uint64_t p) { return (uint32_t)((uint64_t)std::ceil(v / (long double)p) * p); }
@@ -170,6 +181,7 @@ static void build_wino7_invfirst(PrimeConst& pc, uint64_t zeta, uint64_t s, uint
   const Wino7Bounds b = wino7_consts(k, inv_mod(zeta, p), s, p);
   const uint64_t Rm = (1ull << 32) % p;
   k.mu = (uint32_t)mulmod(mulmod(mulmod(7, inv_mod(6, p), p), s, p), Rm, p);
+  shoup_pair(mulmod(mulmod(7, inv_mod(6, p), p), s, p), p, k.mu_w, k.mu_q);
   const long double R2 = b.R2, G = b.G, S7 = b.M0;
   k.k1p = up_p(G, p);
   k.k2p = up_p(3.0L * G, p);
@@ -203,14 +215,18 @@ static void build_wino5(PrimeConst& pc, uint64_t zeta, uint64_t p) {
     std::memset(&k, 0, sizeof(k));
     k.mu = (uint32_t)mulmod(mulmod(W1, i4, p), Rm, p);
     k.rho = cen(mulmod(Wm, i4, p));
+    shoup_pair(mulmod(W1, i4, p), p, k.mu_w, k.mu_q);
+    shoup_pair(mulmod(Wm, i4, p), p, k.rho_w, k.rho_q);
+    k.toff = (uint32_t)(4 * p);  // Tm in (-2X, 2X)
     k.a00 = cen(mulmod(B0, i2, p));
     k.a01 = cen(mulmod(sub(0, B1), i2, p));
     k.a10 = cen(mulmod(B1, i2, p));
     auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
     k.kT = up(2.0L * X * ch);
     k.kG = up(2.0L * X * ch);
-    const long double M0 = std::floor(4.0L * X * (p - 1) / two32) + p;
-    const long double R2 = std::floor(((long double)k.kT + 2.0L * X * ch) / two32) + p;
+    // (bounded by 2p: M0 and R2 may come from the Shoup forms)
+    const long double M0 = std::max(std::floor(4.0L * X * (p - 1) / two32) + p, X);
+    const long double R2 = std::max(std::floor(((long double)k.kT + 2.0L * X * ch) / two32) + p, X);
     const long double G = std::floor(((long double)k.kG + 2.0L * X * ch) / two32) + p;
     k.k1p = (uint32_t)up(R2);
     k.k2p = (uint32_t)up(G);

@@ -32,7 +32,10 @@ struct WinoConst {
   int32_t rho;          // W(-1) / 6 * R
   int32_t a00, a01, a10, b00, b01, b10;  // (X^2 + X + 1) / (X^2 - X + 1) parts, / 6, * R
   uint32_t k1p, k2p, k3p, k4p, k5p;      // output-sum offsets (multiples of p)
-  uint32_t pad;
+  // Shoup forms of the two single-product terms (M0 = S mu, R2 = (Tm + toff) rho): plain
+  // constants and floor(c 2^32 / p); toff = multiple of p making the signed Tm non-negative
+  uint32_t mu_w, mu_q, rho_w, rho_q, toff;
+  uint32_t pad0, pad1;
 };
 
 struct PrimeConst {

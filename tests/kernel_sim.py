@@ -163,6 +163,30 @@ class Prime:
             out[k], out[T - k] = (v, u) if inv else (u, v)
         return out
 
+    def shoup_c(self, x, cw, cq):
+        """shoup_mul by a constant (plain c, floor(c 2^32 / p)): x < 2^32 -> [0, 2p)."""
+        x = np.asarray(x, dtype=U)
+        assert np.all(x < U(1 << 32))
+        q = (x * U(cq)) >> U(32)
+        r = (x * U(cw) - q * self.p) & M32
+        assert np.all(r < U(2) * self.p)
+        return r
+
+    def wino_m0(self, S, w, acc):
+        """keyswitch.cu wino_m0: S mu (Shoup under SFHR_WINO_SHOUP, else Montgomery)."""
+        if WINO_SHOUP:
+            return self.shoup_c(np.asarray(S).astype(U), w.mu_w, w.mu_q)
+        return self.redc(np.asarray(S).astype(U) * U(w.mu))
+
+    def wino_r2(self, Tm, w, acc):
+        """keyswitch.cu wino_r2: Tm rho with Tm offset by toff (a multiple of p) for Shoup."""
+        if WINO_SHOUP:
+            x = np.asarray(Tm, dtype=np.int64) + int(w.toff)
+            assert np.all(x >= 0), "negative Shoup operand"
+            assert int(w.toff) % int(self.p) == 0
+            return self.shoup_c(x.astype(U), w.rho_w, w.rho_q)
+        return self.redc(acc(w.kT, (Tm, w.rho)))
+
     def dft_wino7(self, xs, inv=False, red=False):
         """keyswitch.cu dft_wino7: Rader/Winograd radix-7 DFT, signed operands, its offsets."""
         w = self.wino[1 if inv else 0]
@@ -187,8 +211,8 @@ class Prime:
                 r = r + a * I(c)
             assert np.all(r >= 0), "negative REDC input"
             return r.astype(U)
-        M0 = self.redc(S.astype(U) * U(w.mu))
-        R2 = self.redc(acc(w.kT, (Tm, w.rho)))
+        M0 = self.wino_m0(S, w, acc)
+        R2 = self.wino_r2(Tm, w, acc)
         g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01)))
         g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00)))
         h0 = self.redc(acc(w.kG, (C0, w.b00), (C1, w.b01)))
@@ -225,8 +249,8 @@ class Prime:
                 r = r + a * I(c)
             assert np.all(r >= 0), "negative REDC input"
             return r.astype(U)
-        M0 = self.redc(S.astype(U) * U(w.mu)).astype(I)
-        R2 = self.redc(acc(w.kT, (Tm, w.rho))).astype(I)
+        M0 = self.wino_m0(S, w, acc).astype(I)
+        R2 = self.wino_r2(Tm, w, acc).astype(I)
         g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01))).astype(I)
         g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00))).astype(I)
         X0 = x[0].astype(I) + M0
@@ -260,8 +284,8 @@ class Prime:
                 r = r + a * I(k)
             assert np.all(r >= 0)
             return r.astype(U)
-        S7 = self.redc(S.astype(U) * U(w.mu)).astype(I)
-        R2 = self.redc(acc(w.kT, (Tm, w.rho))).astype(I)
+        S7 = self.wino_m0(S, w, acc).astype(I)
+        R2 = self.wino_r2(Tm, w, acc).astype(I)
         g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01))).astype(I)
         g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00))).astype(I)
         h0 = self.redc(acc(w.kG, (C0, w.b00), (C1, w.b01))).astype(I)
@@ -293,6 +317,7 @@ class Prime:
 LAZY_INV = True   # keyswitch.cu SFHR_LAZY_INV
 LAZY_MAC = True   # keyswitch.cu SFHR_LAZY_MAC (applies from l >= 3)
 SHOUP_MID = True  # keyswitch.cu SFHR_SHOUP_MID (mid-stage twiddles as Shoup products)
+WINO_SHOUP = True  # keyswitch.cu SFHR_WINO_SHOUP (Rader M0 / R2 terms as Shoup products)
 
 
 def forward(sp: SimPlan, pr: Prime, vals, red=True):
