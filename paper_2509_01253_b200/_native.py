@@ -117,7 +117,8 @@ class WinoConst(C.Structure):
     _fields_ = [("kT", C.c_uint64), ("kG", C.c_uint64), ("mu", C.c_uint32), ("rho", C.c_int32)] + \
                [(n, C.c_int32) for n in ("a00", "a01", "a10", "b00", "b01", "b10")] + \
                [(n, C.c_uint32) for n in ("k1p", "k2p", "k3p", "k4p", "k5p", "mu_w", "mu_q", "rho_w",
-                                          "rho_q", "toff", "pad0", "pad1")]
+                                          "rho_q", "toff", "pad0", "pad1")] + \
+               [(n, C.c_int32) for n in ("ka01", "ka10", "kb01", "kb10")]
 
 
 class PrimeConst(C.Structure):

@@ -133,6 +133,33 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
 #ifndef SFHR_WINO_SHOUP
 #define SFHR_WINO_SHOUP 1
 #endif
+#ifndef SFHR_WINO_KARA
+#define SFHR_WINO_KARA 0
+#endif
+// the 2x2 blocks of the Rader DFTs: g = [[a00, a01], [a10, a00]] (A0, A1), h likewise with b,
+// Karatsuba (3 IMAD.WIDE per pair instead of 4; operand ranges unchanged, see WinoConst)
+__device__ __forceinline__ void wino_g(int32_t A0, int32_t A1, const WinoConst& w, uint32_t p, uint32_t pinv,
+                                       uint32_t& g0, uint32_t& g1) {
+  if (SFHR_WINO_KARA) {
+    const int64_t P = (int64_t)(A0 - A1) * w.a00;
+    g0 = redc((uint64_t)((int64_t)w.kG + P + (int64_t)A1 * w.ka01), p, pinv);
+    g1 = redc((uint64_t)((int64_t)w.kG - P + (int64_t)A0 * w.ka10), p, pinv);
+  } else {
+    g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
+    g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
+  }
+}
+__device__ __forceinline__ void wino_h(int32_t C0, int32_t C1, const WinoConst& w, uint32_t p, uint32_t pinv,
+                                       uint32_t& h0, uint32_t& h1) {
+  if (SFHR_WINO_KARA) {
+    const int64_t P = (int64_t)(C0 + C1) * w.b00;
+    h0 = redc((uint64_t)((int64_t)w.kG + P + (int64_t)C1 * w.kb01), p, pinv);
+    h1 = redc((uint64_t)((int64_t)w.kG + P + (int64_t)C0 * w.kb10), p, pinv);
+  } else {
+    h0 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b00 + (int64_t)C1 * w.b01), p, pinv);
+    h1 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b10 + (int64_t)C1 * w.b00), p, pinv);
+  }
+}
 __device__ __forceinline__ uint32_t wino_m0(uint32_t S, const WinoConst& w, uint32_t p, uint32_t pinv) {
   return SFHR_WINO_SHOUP ? shoup_mul(S, make_uint2(w.mu_w, w.mu_q), p) : redc((uint64_t)S * w.mu, p, pinv);
 }
@@ -168,10 +195,9 @@ __device__ __forceinline__ void dft_wino7(const uint32_t (&x)[7], uint32_t (&y)[
   const int32_t C0 = d03 - d25, C1 = d14 + d25;                                     // V mod X^2-X+1
   const uint32_t M0 = wino_m0(S, w, p, pinv);
   const uint32_t R2 = wino_r2(Tm, w, p, pinv);
-  const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
-  const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
-  const uint32_t h0 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b00 + (int64_t)C1 * w.b01), p, pinv);
-  const uint32_t h1 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b10 + (int64_t)C1 * w.b00), p, pinv);
+  uint32_t g0, g1, h0, h1;
+  wino_g(A0, A1, w, p, pinv, g0, g1);
+  wino_h(C0, C1, w, p, pinv, h0, h1);
   // z_i = x_0 + M0 + (-1)^i R2 + g_{i mod 3} +- h_{i mod 3} (g_2 = -g_0 - g_1, h_2 = h_1 - h_0,
   // h negated for i >= 3), mod 2^32 arithmetic whose true values are non-negative
   const uint32_t X0 = x[0] + M0, Xp = X0 + R2, Xm = X0 - R2;
@@ -209,10 +235,9 @@ __device__ __forceinline__ void inv_first7(const uint32_t (&C)[6], uint32_t (&o)
   const int32_t C0 = d03 - d25, C1 = d14 + d25;
   const uint32_t S7 = wino_m0(S, w, p, pinv);  // 7 s S / 6
   const uint32_t R2 = wino_r2(Tm, w, p, pinv);
-  const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
-  const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
-  const uint32_t h0 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b00 + (int64_t)C1 * w.b01), p, pinv);
-  const uint32_t h1 = redc((uint64_t)((int64_t)w.kG + (int64_t)C0 * w.b10 + (int64_t)C1 * w.b00), p, pinv);
+  uint32_t g0, g1, h0, h1;
+  wino_g(A0, A1, w, p, pinv, g0, g1);
+  wino_h(C0, C1, w, p, pinv, h0, h1);
   uint32_t z[6];
   z[0] = S7 + R2 + h0 + w.k1p - g0;
   z[1] = 2 * (R2 + h0);
@@ -236,8 +261,8 @@ __device__ __forceinline__ void dft_wino5(const uint32_t (&x)[5], uint32_t (&y)[
   const int32_t A0 = (int32_t)(v0 - v2), A1 = (int32_t)(v1 - v3);  // V mod X^2 + 1
   const uint32_t M0 = wino_m0(S, w, p, pinv);
   const uint32_t R2 = wino_r2(Tm, w, p, pinv);
-  const uint32_t g0 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a00 + (int64_t)A1 * w.a01), p, pinv);
-  const uint32_t g1 = redc((uint64_t)((int64_t)w.kG + (int64_t)A0 * w.a10 + (int64_t)A1 * w.a00), p, pinv);
+  uint32_t g0, g1;
+  wino_g(A0, A1, w, p, pinv, g0, g1);
   const uint32_t X0 = x[0] + M0, Xp = X0 + R2, Xm = X0 - R2;
   uint32_t z[4];
   z[0] = Xp + g0;

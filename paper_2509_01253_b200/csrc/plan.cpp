@@ -136,6 +136,16 @@ static Wino7Bounds wino7_consts(WinoConst& k, uint64_t z, uint64_t scale, uint64
   k.b00 = cen(mulmod((2 * D0 + D1) % p, i6, p));
   k.b01 = cen(mulmod(sub(D0, D1), i6, p));
   k.b10 = cen(mulmod((D0 + 2 * D1) % p, i6, p));
+  auto cadd = [&](int32_t a, int32_t b) {  // centred Montgomery constants a + b, re-centred
+    int64_t v = ((int64_t)a + b) % (int64_t)p;
+    if (v > (int64_t)(p / 2)) v -= p;
+    if (v < -(int64_t)(p / 2)) v += p;
+    return (int32_t)v;
+  };
+  k.ka01 = cadd(k.a01, k.a00);
+  k.ka10 = cadd(k.a10, k.a00);
+  k.kb01 = cadd(k.b01, -k.b00);
+  k.kb10 = cadd(k.b10, -k.b00);
   // REDC(x) <= floor(x / 2^32) + p; signed sums offset by a multiple of p
   auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
   k.kT = up(Tmax * ch);
@@ -221,13 +231,22 @@ static void build_wino5(PrimeConst& pc, uint64_t zeta, uint64_t p) {
     k.a00 = cen(mulmod(B0, i2, p));
     k.a01 = cen(mulmod(sub(0, B1), i2, p));
     k.a10 = cen(mulmod(B1, i2, p));
+    auto cadd = [&](int32_t a, int32_t b) {
+      int64_t v = ((int64_t)a + b) % (int64_t)p;
+      if (v > (int64_t)(p / 2)) v -= p;
+      if (v < -(int64_t)(p / 2)) v += p;
+      return (int32_t)v;
+    };
+    k.ka01 = cadd(k.a01, k.a00);
+    k.ka10 = cadd(k.a10, k.a00);
     auto up = [&](long double v) { return (uint64_t)std::ceil(v / (long double)p) * p; };
     k.kT = up(2.0L * X * ch);
-    k.kG = up(2.0L * X * ch);
+    // |a00 (A0 - A1)| + |ka A| < (2X + X) ch (Karatsuba form; the direct form needs 2 X ch)
+    k.kG = up(3.0L * X * ch);
     // (bounded by 2p: M0 and R2 may come from the Shoup forms)
     const long double M0 = std::max(std::floor(4.0L * X * (p - 1) / two32) + p, X);
     const long double R2 = std::max(std::floor(((long double)k.kT + 2.0L * X * ch) / two32) + p, X);
-    const long double G = std::floor(((long double)k.kG + 2.0L * X * ch) / two32) + p;
+    const long double G = std::floor(((long double)k.kG + 3.0L * X * ch) / two32) + p;
     k.k1p = (uint32_t)up(R2);
     k.k2p = (uint32_t)up(G);
     k.k3p = (uint32_t)up(R2 + G);

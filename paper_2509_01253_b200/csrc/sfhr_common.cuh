@@ -36,6 +36,10 @@ struct WinoConst {
   // constants and floor(c 2^32 / p); toff = multiple of p making the signed Tm non-negative
   uint32_t mu_w, mu_q, rho_w, rho_q, toff;
   uint32_t pad0, pad1;
+  // Karatsuba forms of the 2x2 blocks (3 products instead of 4 per pair, same ranges):
+  // g0 = a00 (A0 - A1) + ka01 A1, g1 = -a00 (A0 - A1) + ka10 A0  (ka01 = a01 + a00, ka10 = a10 + a00)
+  // h0 = b00 (C0 + C1) + kb01 C1, h1 = b00 (C0 + C1) + kb10 C0   (kb01 = b01 - b00, kb10 = b10 - b00)
+  int32_t ka01, ka10, kb01, kb10;
 };
 
 struct PrimeConst {

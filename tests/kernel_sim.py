@@ -187,6 +187,24 @@ class Prime:
             return self.shoup_c(x.astype(U), w.rho_w, w.rho_q)
         return self.redc(acc(w.kT, (Tm, w.rho)))
 
+    def wino_g(self, A0, A1, w, acc):
+        """keyswitch.cu wino_g: [[a00, a01], [a10, a00]] (A0, A1), Karatsuba under SFHR_WINO_KARA."""
+        if WINO_KARA:
+            D = A0 - A1
+            assert np.all(np.abs(D) < (1 << 31)), "Karatsuba operand overflow"
+            return (self.redc(acc(w.kG, (D, w.a00), (A1, w.ka01))),
+                    self.redc(acc(w.kG, (-D, w.a00), (A0, w.ka10))))
+        return self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01))), self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00)))
+
+    def wino_h(self, C0, C1, w, acc):
+        """keyswitch.cu wino_h: [[b00, b01], [b10, b00]] (C0, C1), Karatsuba under SFHR_WINO_KARA."""
+        if WINO_KARA:
+            S = C0 + C1
+            assert np.all(np.abs(S) < (1 << 31)), "Karatsuba operand overflow"
+            return (self.redc(acc(w.kG, (S, w.b00), (C1, w.kb01))),
+                    self.redc(acc(w.kG, (S, w.b00), (C0, w.kb10))))
+        return self.redc(acc(w.kG, (C0, w.b00), (C1, w.b01))), self.redc(acc(w.kG, (C0, w.b10), (C1, w.b00)))
+
     def dft_wino7(self, xs, inv=False, red=False):
         """keyswitch.cu dft_wino7: Rader/Winograd radix-7 DFT, signed operands, its offsets."""
         w = self.wino[1 if inv else 0]
@@ -213,10 +231,8 @@ class Prime:
             return r.astype(U)
         M0 = self.wino_m0(S, w, acc)
         R2 = self.wino_r2(Tm, w, acc)
-        g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01)))
-        g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00)))
-        h0 = self.redc(acc(w.kG, (C0, w.b00), (C1, w.b01)))
-        h1 = self.redc(acc(w.kG, (C0, w.b10), (C1, w.b00)))
+        g0, g1 = self.wino_g(A0, A1, w, acc)
+        h0, h1 = self.wino_h(C0, C1, w, acc)
         X0 = x[0].astype(I) + M0.astype(I)
         R2, g0, g1, h0, h1 = (a.astype(I) for a in (R2, g0, g1, h0, h1))
         gs, hd = g0 + g1, h1 - h0
@@ -251,8 +267,7 @@ class Prime:
             return r.astype(U)
         M0 = self.wino_m0(S, w, acc).astype(I)
         R2 = self.wino_r2(Tm, w, acc).astype(I)
-        g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01))).astype(I)
-        g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00))).astype(I)
+        g0, g1 = (v.astype(I) for v in self.wino_g(A0, A1, w, acc))
         X0 = x[0].astype(I) + M0
         z = [X0 + R2 + g0, X0 - R2 + w.k1p + g1, X0 + R2 + w.k2p - g0, X0 - R2 + w.k3p - g1]
         for a in z:
@@ -286,10 +301,8 @@ class Prime:
             return r.astype(U)
         S7 = self.wino_m0(S, w, acc).astype(I)
         R2 = self.wino_r2(Tm, w, acc).astype(I)
-        g0 = self.redc(acc(w.kG, (A0, w.a00), (A1, w.a01))).astype(I)
-        g1 = self.redc(acc(w.kG, (A0, w.a10), (A1, w.a00))).astype(I)
-        h0 = self.redc(acc(w.kG, (C0, w.b00), (C1, w.b01))).astype(I)
-        h1 = self.redc(acc(w.kG, (C0, w.b10), (C1, w.b00))).astype(I)
+        g0, g1 = (v.astype(I) for v in self.wino_g(A0, A1, w, acc))
+        h0, h1 = (v.astype(I) for v in self.wino_h(C0, C1, w, acc))
         z = [S7 + R2 + h0 + w.k1p - g0, 2 * (R2 + h0), 2 * R2 + h1 + w.k2p - 2 * g0 - g1,
              g1 + h1 + h0 + w.k3p - g0, 2 * R2 + g1 + h0 + w.k4p - h1 - g0, 2 * h0 + w.k5p - 2 * g0 - g1 - h1]
         out = []
@@ -318,6 +331,7 @@ LAZY_INV = True   # keyswitch.cu SFHR_LAZY_INV
 LAZY_MAC = True   # keyswitch.cu SFHR_LAZY_MAC (applies from l >= 3)
 SHOUP_MID = True  # keyswitch.cu SFHR_SHOUP_MID (mid-stage twiddles as Shoup products)
 WINO_SHOUP = True  # keyswitch.cu SFHR_WINO_SHOUP (Rader M0 / R2 terms as Shoup products)
+WINO_KARA = False  # keyswitch.cu SFHR_WINO_KARA (Karatsuba 2x2 blocks)
 
 
 def forward(sp: SimPlan, pr: Prime, vals, red=True):
