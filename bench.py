@@ -335,7 +335,7 @@ def stage_traffic(N):
     algorithmic 32 N bytes per row (rows = grid / 3 CTAs per cluster); the capture
     is of the b = 12 (N = 2058) ResNet-20 stem pack, so the ratio is only quoted
     for that ring."""
-    f = ROOT / "profiles" / "r02_ncu_stage_final_summary.json"
+    f = ROOT / "profiles" / "r02g" / "ncu_stage_summary.json"
     try:
         launches = [l for l in json.loads(f.read_text())["launches"] if "ks_stage_kernel" in l["kernel"]]
     except Exception:
@@ -343,7 +343,7 @@ def stage_traffic(N):
     tr = [1e6 * (l["dram__bytes_read.sum"] + l["dram__bytes_write.sum"]) for l in launches]
     alg = [l["launch__grid_size"] / 3 * 32 * 2058 for l in launches]
     out = {"traffic": sum(tr) / len(tr), "unit": "bytes per launch", "launches": len(tr),
-           "algorithmic_bytes_per_launch": sum(alg) / len(alg), "source": f"profiles/{f.name}"}
+           "algorithmic_bytes_per_launch": sum(alg) / len(alg), "source": str(f.relative_to(ROOT))}
     # the compute side of the same capture: this kernel is bound by the integer-multiply pipe
     # (IMAD / IMAD.HI / IMAD.WIDE run only on fmaheavy), not by HBM
     def mean(key):
