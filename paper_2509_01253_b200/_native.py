@@ -125,7 +125,8 @@ class PrimeConst(C.Structure):
     _fields_ = [("p", C.c_uint32), ("pinv", C.c_uint32), ("mu", C.c_uint32), ("r2", C.c_uint32),
                 ("rmod", C.c_uint32), ("z", (C.c_uint32 * 7) * 7), ("zi", (C.c_uint32 * 7) * 7),
                 ("g", (C.c_uint32 * 7) * 7), ("hc", (C.c_uint32 * 3) * 3), ("hs", (C.c_uint32 * 3) * 3),
-                ("q_mod64", C.c_uint64), ("inv_p", C.c_double), ("wino", WinoConst * 3)]
+                ("q_mod64", C.c_uint64), ("inv_p", C.c_double), ("wino", WinoConst * 3),
+                ("bc", C.c_uint32), ("pad_bc", C.c_uint32)]
 
 
 class RingConst(C.Structure):

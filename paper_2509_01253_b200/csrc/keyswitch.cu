@@ -65,6 +65,14 @@ struct Geo {
 // small DFT helper (constants come from the __grid_constant__ parameter block
 // at compile-time offsets -> uniform-register operands of IMAD.WIDE.U32)
 
+// Barrett step to [0, 2p) (A/B knob: the 32-bit-multiply form bred or umulhi by floor(2^32 / p))
+#ifndef SFHR_BRED
+#define SFHR_BRED 1
+#endif
+__device__ __forceinline__ uint32_t bar(uint32_t y, const PrimeConst& pc) {
+  return SFHR_BRED ? bred(y, pc.p, pc.bc) : y - __umulhi(y, pc.mu) * pc.p;
+}
+
 template <int T>
 __device__ __forceinline__ void dft_t(const uint32_t (&x)[T], uint32_t (&y)[T],
                                       const uint32_t (&Z)[MAXT][MAXT], uint32_t p, uint32_t pinv) {
@@ -95,7 +103,7 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
     b[m - 1] = x[m] + p2 - x[T - m];
     y0 += a[m - 1];
   }
-  y[0] = y0 - __umulhi(y0, mu) * p;
+  y[0] = bar(y0, pc);
 #pragma unroll
   for (int k = 1; k <= H; ++k) {
     uint64_t sp = 0, sq = 0;
@@ -108,8 +116,8 @@ __device__ __forceinline__ void dft_sym(const uint32_t (&x)[T], uint32_t (&y)[T]
     const uint32_t t0 = x[0] + P;
     uint32_t u = t0 + Q, v = t0 + p2 - Q;
     if (RED) {
-      u -= __umulhi(u, mu) * p;
-      v -= __umulhi(v, mu) * p;
+      u = bar(u, pc);
+      v = bar(v, pc);
     }
     y[k] = INV ? v : u;
     y[T - k] = INV ? u : v;
@@ -210,11 +218,11 @@ __device__ __forceinline__ void dft_wino7(const uint32_t (&x)[7], uint32_t (&y)[
   z[4] = Xp + w.k4p + g1 - h1;
   z[5] = Xm + w.k5p - gs - hd;
   const uint32_t y0 = x[0] + S;
-  y[0] = y0 - __umulhi(y0, mu) * p;
+  y[0] = bar(y0, pc);
   // outputs y_{3^i mod 7}
   constexpr int kout[6] = {1, 3, 2, 6, 4, 5};
 #pragma unroll
-  for (int i = 0; i < 6; ++i) y[kout[i]] = RED ? z[i] - __umulhi(z[i], mu) * p : z[i];
+  for (int i = 0; i < 6; ++i) y[kout[i]] = RED ? bar(z[i], pc) : z[i];
 }
 
 // forward DFT whose k >= 1 outputs are multiplied by twiddles next (lazy [0, 6p) ok)
@@ -246,7 +254,7 @@ __device__ __forceinline__ void inv_first7(const uint32_t (&C)[6], uint32_t (&o)
   z[4] = 2 * R2 + g1 + h0 + w.k4p - h1 - g0;
   z[5] = 2 * h0 + w.k5p - 2 * g0 - g1 - h1;
 #pragma unroll
-  for (int j = 0; j < 6; ++j) o[j] = fully(z[j] - __umulhi(z[j], mu) * p, p);
+  for (int j = 0; j < 6; ++j) o[j] = fully(bar(z[j], pc), p);
 }
 
 // Rader radix-5 DFT (plan.cpp build_wino5): 6 IMAD.WIDE + 4 REDC against 8 + 4 for dft_sym.
@@ -270,10 +278,10 @@ __device__ __forceinline__ void dft_wino5(const uint32_t (&x)[5], uint32_t (&y)[
   z[2] = Xp + w.k2p - g0;
   z[3] = Xm + w.k3p - g1;
   const uint32_t y0 = x[0] + S;
-  y[0] = y0 - __umulhi(y0, mu) * p;
+  y[0] = bar(y0, pc);
   constexpr int kout[4] = {1, 2, 4, 3};  // outputs y_{2^i mod 5}
 #pragma unroll
-  for (int i = 0; i < 4; ++i) y[kout[i]] = RED ? z[i] - __umulhi(z[i], mu) * p : z[i];
+  for (int i = 0; i < 4; ++i) y[kout[i]] = RED ? bar(z[i], pc) : z[i];
 }
 
 template <int T>
@@ -427,7 +435,7 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
       const int e1 = step * j;
       uint32_t z[T], x[T];
       // lazy: v[0] is some earlier stage's unreduced output (< 2^32)
-      z[0] = SFHR_LAZY_INV ? v[0] - __umulhi(v[0], pc.mu) * pc.p : v[0];
+      z[0] = SFHR_LAZY_INV ? bar(v[0], pc) : v[0];
       if constexpr (SH) {
         const int es = stepT * j;  // omega^(M - e1 k) = sh[n1 - es k]
 #pragma unroll
@@ -705,8 +713,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       for (int k = 0; k < T; ++k) {
         uint32_t ra = redc(ta[k], p, pinv), rb2 = redc(tb[k], p, pinv);
         if constexpr (kLazyMac<L>) {
-          ra -= __umulhi(ra, mu) * p;
-          rb2 -= __umulhi(rb2, mu) * p;
+          ra = bar(ra, pc);
+          rb2 = bar(rb2, pc);
         }
         aa[k] = r > rb ? aa[k] + ra : ra;
         ab[k] = r > rb ? ab[k] + rb2 : rb2;
@@ -729,8 +737,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 #pragma unroll
     for (int k = 0; k < T; ++k) {
       const uint32_t va = S.acc[item * T + k], vb = S.acc[N + item * T + k];
-      za[k] = va - __umulhi(va, mu) * p;  // -> [0, 2p)
-      zb[k] = vb - __umulhi(vb, mu) * p;
+      za[k] = bar(va, pc);  // -> [0, 2p)
+      zb[k] = bar(vb, pc);
     }
     dft_inv<T>(za, xa, pc);
     dft_inv<T>(zb, xb, pc);

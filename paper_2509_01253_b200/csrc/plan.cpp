@@ -385,6 +385,8 @@ Plan make_plan(int t, int alpha, int p_bits, int D, int l, int gamma, int beta) 
     for (int it = 0; it < 5; ++it) inv *= 2u - (uint32_t)p * inv;  // Newton: p^-1 mod 2^32
     pc.pinv = inv;
     pc.mu = (uint32_t)(R32 / p);
+    pc.bc = (uint32_t)((R32 << 1) / p);
+    if (p < (1ull << 18)) throw std::invalid_argument("NTT prime below 2^18 (bred range)");
     pc.rmod = (uint32_t)(R32 % p);
     pc.r2 = (uint32_t)mulmod(R32 % p, R32 % p, p);
     uint64_t omega = 0;

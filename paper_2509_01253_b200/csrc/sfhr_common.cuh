@@ -56,6 +56,8 @@ struct PrimeConst {
   uint64_t q_mod64;         // (P / p) mod 2^64
   double inv_p;             // 1.0 / p
   WinoConst wino[3];        // t = 7: forward, inverse, inverse first step (t = 5: [0], [1])
+  uint32_t bc;              // floor(2^33 / p): Barrett step with 32-bit multiplies only (bred)
+  uint32_t pad_bc;
 };
 
 struct RingConst {
@@ -103,6 +105,14 @@ __device__ __forceinline__ uint32_t redc_wide(uint64_t x, uint32_t p, uint32_t p
 // a in [0, 2p), bm = b*R mod p  ->  a*b mod p in (0, 2p)
 __device__ __forceinline__ uint32_t mont_mul(uint32_t a, uint32_t bm, uint32_t p, uint32_t pinv) {
   return redc((uint64_t)a * bm, p, pinv);
+}
+
+// Barrett step to [0, 2p) for any y < 2^32 with two low multiplies instead of IMAD.HI + IMAD:
+// q = ((y >> 16) bc) >> 17 with bc = floor(2^33 / p) satisfies y / p - 1/2 - 2^16 / p < q <= y / p
+// (needs 2^18 <= p < 2^31; the product stays below 2^49 / p < 2^32), so y - q p is in [0, 2p)
+__device__ __forceinline__ uint32_t bred(uint32_t y, uint32_t p, uint32_t bc) {
+  const uint32_t q = ((y >> 16) * bc) >> 17;
+  return y - q * p;
 }
 
 // Shoup: x < 2^32, wq = (w, floor(w 2^32 / p)), w < p  ->  x w mod p in [0, 2p)

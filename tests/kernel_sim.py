@@ -54,6 +54,8 @@ class Prime:
     def __init__(self, sp: SimPlan, i: int):
         pc = sp.rc.pc[i]
         self.p, self.pinv, self.mu = U(pc.p), U(pc.pinv), U(pc.mu)
+        self.bc = U(pc.bc)
+        assert int(self.bc) == (1 << 33) // int(self.p)
         self.r2, self.rmod = U(pc.r2), U(pc.rmod)
         T = sp.t
         self.z = np.array([[pc.z[k][m] for m in range(T)] for k in range(T)], dtype=U)
@@ -133,9 +135,15 @@ class Prime:
         return out
 
     def barrett(self, v):
+        """keyswitch.cu bar(): bred (32-bit multiplies) under SFHR_BRED, else umulhi by mu."""
         v = np.asarray(v, dtype=U)
         assert np.all(v < U(1 << 32))
-        r = v - ((v * self.mu) >> U(32)) * self.p
+        if BRED:
+            q = (((v >> U(16)) * self.bc) & M32) >> U(17)
+            assert np.all(((v >> U(16)) * self.bc) < U(1 << 32))
+            r = (v - q * self.p) & M32
+        else:
+            r = v - ((v * self.mu) >> U(32)) * self.p
         assert np.all(r < U(2) * self.p)
         return r
 
@@ -331,6 +339,7 @@ LAZY_INV = True   # keyswitch.cu SFHR_LAZY_INV
 LAZY_MAC = True   # keyswitch.cu SFHR_LAZY_MAC (applies from l >= 3)
 SHOUP_MID = True  # keyswitch.cu SFHR_SHOUP_MID (mid-stage twiddles as Shoup products)
 WINO_SHOUP = True  # keyswitch.cu SFHR_WINO_SHOUP (Rader M0 / R2 terms as Shoup products)
+BRED = True        # keyswitch.cu SFHR_BRED (Barrett step with 32-bit multiplies)
 WINO_KARA = False  # keyswitch.cu SFHR_WINO_KARA (Karatsuba 2x2 blocks)
 
 
@@ -443,8 +452,7 @@ def stage_row(sp: SimPlan, x, reps_dinv_keys, identity, decompose, automorph_u64
             accA = accA + ra
             accB = accB + rb
             assert np.all(accA < U(1 << 32)) and np.all(accB < U(1 << 32))
-        barrett = lambda v: v - ((v * pr.mu) >> U(32)) * pr.p  # noqa: E731
-        za, zb = barrett(accA), barrett(accB)
+        za, zb = pr.barrett(accA), pr.barrett(accB)
         assert np.all(za < U(2) * pr.p) and np.all(zb < U(2) * pr.p)
         ya = inverse(sp, pr, za)
         yb = inverse(sp, pr, zb)
