@@ -363,6 +363,12 @@ constexpr bool kItemMajor = T <= 5;
 #ifndef SFHR_SHOUP_MID
 #define SFHR_SHOUP_MID 1
 #endif
+// twiddles loaded before the item's DFT instead of between its stores (the compiler cannot hoist
+// shared loads above stores to the transform buffer it cannot prove disjoint): the LDS latency
+// overlaps the DFT instead of stalling the twiddle multiplies
+#ifndef SFHR_TW_EARLY
+#define SFHR_TW_EARLY 1
+#endif
 
 // forward DIF stages s = 0 .. alpha-3 (all but the last, span > 1).  SH: twiddles from the Shoup
 // pairs sh[e / t] (every mid-stage exponent is a multiple of t) instead of the Montgomery table
@@ -381,6 +387,19 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
     auto item = [&](uint32_t* v, const int j) {
       const int e1 = step * j;
       uint32_t x[T], y[T];
+      if constexpr (SH && SFHR_TW_EARLY) {
+        const int es = stepT * j;  // e1 / t
+        uint2 tw[T];
+#pragma unroll
+        for (int k = 1; k < T; ++k) tw[k] = sh[es * k];
+#pragma unroll
+        for (int m = 0; m < T; ++m) x[m] = v[m * L];
+        dft_fwd_tw<T>(x, y, pc);
+        v[0] = y[0];
+#pragma unroll
+        for (int k = 1; k < T; ++k) v[k * L] = shoup_mul(y[k], tw[k], pc.p);
+        return;
+      }
 #pragma unroll
       for (int m = 0; m < T; ++m) x[m] = v[m * L];
       dft_fwd_tw<T>(x, y, pc);
@@ -624,6 +643,11 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
         const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
         uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
         int dg[L][T - 1];
+        uint32_t tw[T];  // first-step twists omega^(q m), shared by the l digit transforms
+        if (SFHR_TW_EARLY) {
+#pragma unroll
+          for (int q = 1; q < T; ++q) tw[q] = S.wt[q * m];
+        }
 #pragma unroll
         for (int j = 0; j < T - 1; ++j) {
           const uint64_t v1 = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
@@ -647,7 +671,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
           xv[T - 1] = 0;
           dft_fwd_tw<T>(xv, yq, pc);
 #pragma unroll
-          for (int q = 1; q < T; ++q) o[(q - 1) * n1] = mont_mul(yq[q], S.wt[q * m], p, pinv);
+          for (int q = 1; q < T; ++q) o[(q - 1) * n1] = mont_mul(yq[q], SFHR_TW_EARLY ? tw[q] : S.wt[q * m], p, pinv);
 #else
 #pragma unroll
           for (int q = 1; q < T; ++q) {
