@@ -36,6 +36,17 @@
 #ifndef SFHR_FUSED_FIRST_STEP
 #define SFHR_FUSED_FIRST_STEP 1
 #endif
+// row prologue by bulk copies (one elected thread, one mbarrier) instead of a 16-byte
+// load/store loop per thread: the mask and the twiddle tables arrive in one round trip
+#ifndef SFHR_STAGE_BULK
+#define SFHR_STAGE_BULK 1
+#endif
+// L2 CRT path: the body x.b is bulk-copied into the dead accumulator region while the inverse
+// transforms run, and the identity term reads the staged mask, so the last arriver's body
+// gathers and identity loads hit shared memory instead of global
+#ifndef SFHR_BODY_STAGE
+#define SFHR_BODY_STAGE 1
+#endif
 
 namespace cg = cooperative_groups;
 
@@ -326,6 +337,29 @@ __device__ __forceinline__ uint32_t lift_signed(int d, uint32_t p) {
   return d < 0 ? (uint32_t)(d + (int)p) : (uint32_t)d;
 }
 
+// bulk-copy helpers (cp.async.bulk completes on an mbarrier; sizes and addresses are 16-byte
+// multiples: rows are 2N u64 with N even, the twiddle rows are padded to 4 words)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void row_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void row_bar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void row_bar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------
 // transform building blocks over nb buffers of N words each (block-wide)
 
@@ -563,7 +597,32 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   // stage x.a (16-byte loads) and the twiddle table; detect an all-zero row
   // (the body is only read when the mask is all zero, which is rare)
   int nz = 0;
-  {
+  // phase 0: the prologue copies; phase 1: the body copy of the L2 CRT path
+  __shared__ __align__(8) uint64_t row_bar_s;
+  __shared__ int last_s;
+  const uint32_t row_bar = smem_addr(&row_bar_s);
+  if (SFHR_STAGE_BULK) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(row_bar) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      const uint32_t xb = (uint32_t)N * 8u;
+      const uint32_t wb = stage_twiddles ? (uint32_t)twid_stride(M) * 4u : 0u;
+      const uint32_t hb = stage_twiddles && SFHR_SHOUP_MID ? (uint32_t)shoup_stride(n1) * 4u : 0u;
+      row_bar_expect(row_bar, xb + wb + hb);
+      row_bulk(smem_addr(S.xa), xin, xb, row_bar);
+      if (wb) row_bulk(smem_addr(S.wt), a.twid + (size_t)PR * twid_stride(M), wb, row_bar);
+      if (hb)
+        row_bulk(smem_addr(S.sh), a.twid + (size_t)rc.np * twid_stride(M) + (size_t)PR * shoup_stride(n1), hb,
+                 row_bar);
+    }
+    __syncthreads();  // the barrier's init is visible
+    row_bar_wait(row_bar, 0);
+    const uint4* src = reinterpret_cast<const uint4*>(S.xa);
+    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {
+      const uint4 v = src[c];
+      nz |= (v.x | v.y | v.z | v.w) != 0;
+    }
+  } else {
     const uint4* src = reinterpret_cast<const uint4*>(xin);  // rows are 16-byte aligned (N even)
     uint4* dst = reinterpret_cast<uint4*>(S.xa);
     for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {
@@ -572,7 +631,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       nz |= (v.x | v.y | v.z | v.w) != 0;
     }
   }
-  if (stage_twiddles) {
+  if (stage_twiddles && !SFHR_STAGE_BULK) {
     const uint4* wsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)PR * twid_stride(M));
     uint4* wdst = reinterpret_cast<uint4*>(S.wt);
     for (int k = threadIdx.x; k < twid_stride(M) / 4; k += blockDim.x) wdst[k] = wsrc[k];
@@ -773,8 +832,18 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
   }
   __syncthreads();
+  // the accumulators are dead: stage the body x.b (N u64 = the 2N u32 of S.acc) behind the
+  // inverse transforms (every CTA waits for it before it exits: the copy targets its smem)
+  constexpr bool kBodyStage = SFHR_BODY_STAGE && SFHR_STAGE_BULK;
+  const bool body_staged = kBodyStage && a.crt_scratch != nullptr;
+  if (body_staged && threadIdx.x == 0) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of S.acc before
+    row_bar_expect(row_bar, (uint32_t)N * 8u);
+    row_bulk(smem_addr(S.acc), xin + N, (uint32_t)N * 8u, row_bar);
+  }
   inv_mid_stages<T, A, PR, SFHR_SHOUP_MID>(S.buf, 2, rc, S.wt, S.sh);
   inv_first_step<T, A, PR>(S.buf, 2, rc, S.wt);
+  const uint64_t* xbs = reinterpret_cast<const uint64_t*>(S.acc);  // staged body (body_staged)
 
   // body term x.b + sum_r aut_r(x.b) of coefficient k, gathered from global
   auto body_sum = [&](const int k) -> uint64_t {
@@ -811,7 +880,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     return bsum;
   };
   // explicit CRT of coefficient k from the np CRT-weighted residues (ya_i, yb_i)
-  auto crt_out = [&](const int k, const uint32_t* ya, const uint32_t* yb, const uint64_t bsum) {
+  auto crt_out = [&](const int k, const uint32_t* ya, const uint32_t* yb, const uint64_t bsum,
+                     const bool xa_staged = false) {
     uint64_t ua = 0, ub = 0;
     double fa = 0.0, fb = 0.0;
 #pragma unroll
@@ -825,7 +895,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
     const uint64_t Av = ua - (uint64_t)__double2ll_rn(fa) * rc.P_mod64;
     const uint64_t Bv = ub - (uint64_t)__double2ll_rn(fb) * rc.P_mod64;
-    xout[k] = ((a.identity ? xin[k] : 0ull) - Av) & QMASK;
+    xout[k] = ((a.identity ? (xa_staged ? S.xa[k] : xin[k]) : 0ull) - Av) & QMASK;
     xout[N + k] = (bsum - Bv) & QMASK;
   };
 
@@ -841,15 +911,29 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
     // release: the barrier orders the CTA's stores before thread 0's gpu-scope fence (cumulative)
     __syncthreads();
-    uint32_t* flag = reinterpret_cast<uint32_t*>(S.acc);  // free after the inverse transforms
     if (threadIdx.x == 0) {
       // acq_rel: releases this CTA's residues and, for the last arriver, acquires the peers'
       unsigned old;
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.crt_cnt + row) : "memory");
-      flag[0] = old == (unsigned)(rc.np - 1);
+      last_s = old == (unsigned)(rc.np - 1);
     }
     __syncthreads();
-    if (!flag[0]) return;
+    if (body_staged) row_bar_wait(row_bar, 1);  // every CTA: the copy targets its smem
+    if (!last_s) return;
+    // staged body term x.b + sum_r aut_r(x.b) of coefficient k (shared-memory gathers)
+    auto body_sum_s = [&](const int k) -> uint64_t {
+      uint64_t bsum = a.identity ? xbs[k] : 0ull;
+      const uint32_t kmod = (uint32_t)(k % n1);
+      for (int r = 0; r < a.nreps; ++r) {
+        const uint32_t dinv = a.dinv[r];
+        const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
+        const uint32_t s2 = fastmod((uint32_t)(N + kmod) * dinv, M, rc.magicM);
+        uint64_t v = s1 < (uint32_t)N ? xbs[s1] : 0ull;
+        if (s2 < (uint32_t)N) v -= xbs[s2];
+        bsum += v;
+      }
+      return bsum;
+    };
     for (int k = threadIdx.x; k < N; k += blockDim.x) {
       uint32_t ya[MAXNP], yb[MAXNP];
 #pragma unroll
@@ -859,7 +943,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
           yb[i] = i == PR ? S.buf[N + k] : __ldcg(rs + (size_t)i * 2 * N + N + k);
         }
       }
-      crt_out(k, ya, yb, body_sum(k));
+      crt_out(k, ya, yb, body_staged ? body_sum_s(k) : body_sum(k), body_staged);
     }
     __syncthreads();
     // the row's residues are dead: drop their L2 lines without writing them back
