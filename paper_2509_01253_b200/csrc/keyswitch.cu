@@ -582,9 +582,22 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst
   return s;
 }
 
+// bulk-copy completion state of a CTA across its rows: bar_mask completes the row prologue (or
+// the previous row's prefetch of this row's mask), bar_body the body copy of the L2 CRT path
+struct RowSync {
+  uint32_t bar_mask, bar_body;
+  uint32_t ph_mask, ph_body;  // parity of the next phase to wait for
+  bool prefetched;            // this row's mask was issued by the previous row
+};
+
+#ifndef SFHR_PREFETCH_NEXT
+#define SFHR_PREFETCH_NEXT 1
+#endif
+
 template <int T, int A, int L, int PR>
 __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& a, unsigned char* smem,
-                                          const int64_t row, const bool stage_twiddles, const int split = 0) {
+                                          const int64_t row, const bool stage_twiddles, RowSync& sync,
+                                          const int64_t next_row = -1, const int split = 0) {
   const PrimeConst& pc = rc.pc[PR];
   const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
   const Geo<T, A> g(rc);
@@ -597,14 +610,10 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   // stage x.a (16-byte loads) and the twiddle table; detect an all-zero row
   // (the body is only read when the mask is all zero, which is rare)
   int nz = 0;
-  // phase 0: the prologue copies; phase 1: the body copy of the L2 CRT path
-  __shared__ __align__(8) uint64_t row_bar_s;
   __shared__ int last_s;
-  const uint32_t row_bar = smem_addr(&row_bar_s);
+  const uint32_t row_bar = sync.bar_mask;
   if (SFHR_STAGE_BULK) {
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(row_bar) : "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    if (threadIdx.x == 0 && !sync.prefetched) {
       const uint32_t xb = (uint32_t)N * 8u;
       const uint32_t wb = stage_twiddles ? (uint32_t)twid_stride(M) * 4u : 0u;
       const uint32_t hb = stage_twiddles && SFHR_SHOUP_MID ? (uint32_t)shoup_stride(n1) * 4u : 0u;
@@ -615,8 +624,9 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
         row_bulk(smem_addr(S.sh), a.twid + (size_t)rc.np * twid_stride(M) + (size_t)PR * shoup_stride(n1), hb,
                  row_bar);
     }
-    __syncthreads();  // the barrier's init is visible
-    row_bar_wait(row_bar, 0);
+    row_bar_wait(row_bar, sync.ph_mask);
+    sync.ph_mask ^= 1u;
+    sync.prefetched = false;
     const uint4* src = reinterpret_cast<const uint4*>(S.xa);
     for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {
       const uint4 v = src[c];
@@ -761,6 +771,15 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     // ---- B: first step + mid stages of the l digit transforms ----
     fwd_first_step<T, A, PR>(S.buf, L, rc, S.wt);
 #endif
+    // the mask is dead after the last rep's gathers: prefetch the CTA's next row into it
+    if (SFHR_STAGE_BULK && SFHR_PREFETCH_NEXT && next_row >= 0 && r == re - 1 && a.crt_scratch && !a.acc_out) {
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of S.xa before
+        row_bar_expect(sync.bar_mask, (uint32_t)N * 8u);
+        row_bulk(smem_addr(S.xa), a.in + next_row * 2 * (int64_t)N, (uint32_t)N * 8u, sync.bar_mask);
+      }
+      sync.prefetched = true;
+    }
     fwd_mid_stages<T, A, PR, SFHR_SHOUP_MID>(S.buf, L, rc, S.wt, S.sh);
     // the staged mask is dead after the last rep's gathers: tell the peers they may push
     // their CRT residues into it (the matching wait precedes our own pushes)
@@ -838,8 +857,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   const bool body_staged = kBodyStage && a.crt_scratch != nullptr;
   if (body_staged && threadIdx.x == 0) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of S.acc before
-    row_bar_expect(row_bar, (uint32_t)N * 8u);
-    row_bulk(smem_addr(S.acc), xin + N, (uint32_t)N * 8u, row_bar);
+    row_bar_expect(sync.bar_body, (uint32_t)N * 8u);
+    row_bulk(smem_addr(S.acc), xin + N, (uint32_t)N * 8u, sync.bar_body);
   }
   inv_mid_stages<T, A, PR, SFHR_SHOUP_MID>(S.buf, 2, rc, S.wt, S.sh);
   inv_first_step<T, A, PR>(S.buf, 2, rc, S.wt);
@@ -918,7 +937,10 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       last_s = old == (unsigned)(rc.np - 1);
     }
     __syncthreads();
-    if (body_staged) row_bar_wait(row_bar, 1);  // every CTA: the copy targets its smem
+    if (body_staged) {  // every CTA: the copy targets its smem
+      row_bar_wait(sync.bar_body, sync.ph_body);
+      sync.ph_body ^= 1u;
+    }
     if (!last_s) return;
     // staged body term x.b + sum_r aut_r(x.b) of coefficient k (shared-memory gathers)
     auto body_sum_s = [&](const int k) -> uint64_t {
@@ -943,7 +965,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
           yb[i] = i == PR ? S.buf[N + k] : __ldcg(rs + (size_t)i * 2 * N + N + k);
         }
       }
-      crt_out(k, ya, yb, body_staged ? body_sum_s(k) : body_sum(k), body_staged);
+      crt_out(k, ya, yb, body_staged ? body_sum_s(k) : body_sum(k), body_staged && !sync.prefetched);
     }
     __syncthreads();
     // the row's residues are dead: drop their L2 lines without writing them back
@@ -999,15 +1021,27 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 // a cluster processes SFHR_ROWS_PER_CLUSTER consecutive rows (twiddles staged once)
 template <int T, int A, int L, int PR>
 __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem, const int64_t item) {
+  __shared__ __align__(8) uint64_t bars[2];
+  RowSync sync{smem_addr(&bars[0]), smem_addr(&bars[1]), 0u, 0u, false};
+  if (SFHR_STAGE_BULK) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sync.bar_mask) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sync.bar_body) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    __syncthreads();  // the barriers' init is visible
+  }
   if (a.acc_out && a.nsplit > 1) {  // representative split: item = (row, split)
     const unsigned r = (unsigned)item / (unsigned)a.nsplit;
-    stage_row<T, A, L, PR>(rc, a, smem, r, true, (int)((unsigned)item - r * (unsigned)a.nsplit));
+    stage_row<T, A, L, PR>(rc, a, smem, r, true, sync, -1, (int)((unsigned)item - r * (unsigned)a.nsplit));
     return;
   }
   const int64_t row0 = item * SFHR_ROWS_PER_CLUSTER;
   for (int rr = 0; rr < SFHR_ROWS_PER_CLUSTER; ++rr) {
     if (row0 + rr >= a.B) break;  // uniform across the cluster
-    stage_row<T, A, L, PR>(rc, a, smem, row0 + rr, rr == 0);
+    if (rr > 0) __syncthreads();  // the previous row's last shared-memory reads are done
+    const int64_t next = rr + 1 < SFHR_ROWS_PER_CLUSTER && row0 + rr + 1 < a.B ? row0 + rr + 1 : -1;
+    stage_row<T, A, L, PR>(rc, a, smem, row0 + rr, rr == 0, sync, next);
   }
 }
 
@@ -1042,7 +1076,9 @@ __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMin
     // prime-major groups of `group` items: the CTAs resident at any time run one or two of the
     // np prime specialisations of this kernel, not all of them (instruction-cache footprint)
     // (32-bit: the grid has < 2^31 CTAs; 64-bit divisions here cost ~1 % of the instructions)
-    const unsigned nitems = (unsigned)(a.acc_out && a.nsplit > 1 ? a.B * a.nsplit : a.B);
+    const unsigned nitems = (unsigned)(a.acc_out && a.nsplit > 1
+                                           ? a.B * a.nsplit
+                                           : (a.B + SFHR_ROWS_PER_CLUSTER - 1) / SFHR_ROWS_PER_CLUSTER);
     const unsigned per_group = (unsigned)a.group * (unsigned)rc.np;
     const unsigned g = blockIdx.x / per_group, base = g * (unsigned)a.group;
     const unsigned gc = nitems - base < (unsigned)a.group ? nitems - base : (unsigned)a.group;
