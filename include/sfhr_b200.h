@@ -78,14 +78,16 @@ int sfhr_automorphism_batch(sfhr_ctx* ctx, uint32_t d, const uint64_t* in, uint6
 
 /* KeySwitchEngine.switch_batch (reference crypto.py:404-421): `in` is the
  * already-automorphed batch.  counter (DEVICE u64, may be NULL) is increased
- * by the number of switched rows (live rows only when skip_zero). */
+ * by the number of switched rows (live rows only when skip_zero).  in and out
+ * must not alias and must be 16-byte aligned (SFHR_EINVAL otherwise). */
 int sfhr_keyswitch_batch(sfhr_ctx* ctx, const sfhr_key* key, uint32_t d, const uint64_t* in,
                          uint64_t* out, int64_t B, int skip_zero,
                          unsigned long long* counter, void* stream);
 
 /* tracepack._apply_stage_batch (reference tracepack.py:268-285):
  * out = in + sum_{rep in reps[1:]} KS_rep(aut_rep(in)).  reps: host array
- * (reps[0] must be 1).  in and out must not alias. */
+ * (reps[0] must be 1).  in and out must not alias and must be 16-byte
+ * aligned. */
 int sfhr_stage_batch(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, int nreps,
                      const uint64_t* in, uint64_t* out, int64_t B, int skip_zero,
                      unsigned long long* counter, void* stream);

@@ -658,6 +658,8 @@ int sfhr_keyswitch_batch(sfhr_ctx* ctx, const sfhr_key* key, uint32_t d, const u
   if (!ctx || !key) return fail(SFHR_EINVAL, "null argument");
   if (B == 0) return SFHR_OK;
   if (in == out) return fail(SFHR_EINVAL, "in and out must not alias");
+  // the stage kernel bulk-copies rows into shared memory (cp.async.bulk: 16-byte granules)
+  if (((uintptr_t)in | (uintptr_t)out) & 15) return fail(SFHR_EINVAL, "in and out must be 16-byte aligned");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g(ctx->device);
   uint32_t reps[1] = {d};
@@ -670,6 +672,8 @@ int sfhr_stage_batch(sfhr_ctx* ctx, const sfhr_key* key, const uint32_t* reps, i
   if (!ctx || !key || !reps || nreps < 1) return fail(SFHR_EINVAL, "bad argument");
   if (B == 0) return SFHR_OK;
   if (in == out) return fail(SFHR_EINVAL, "in and out must not alias");
+  // the stage kernel bulk-copies rows into shared memory (cp.async.bulk: 16-byte granules)
+  if (((uintptr_t)in | (uintptr_t)out) & 15) return fail(SFHR_EINVAL, "in and out must be 16-byte aligned");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g(ctx->device);
   try {

@@ -50,7 +50,9 @@ def _as_dev(x, ctx: RingContext):
     if isinstance(x, torch.Tensor):
         if x.device != ctx.dev or x.dtype != torch.int64:
             raise ValueError("device batches must be int64 tensors on the engine's device")
-        return x.contiguous(), False
+        x = x.contiguous()
+        # the C-ABI takes 16-byte aligned rows (bulk copies); a view at an odd u64 offset is copied
+        return (x.clone() if x.data_ptr() % 16 else x), False
     x = np.ascontiguousarray(np.asarray(x, dtype=np.uint64))
     return to_dev(x, ctx.dev), True
 

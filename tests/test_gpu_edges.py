@@ -191,3 +191,26 @@ def test_extract_multi_chunk_ragged(b, gamma, E_frac):
         cnt = min(R.N, E - j * R.N)
         ob = opk.Bundle(gamma, {d: oks.Ct(power[j, q, 0], power[j, q, 1]) for q, d in enumerate(exps)})
         assert np.array_equal(rows[j * R.N:j * R.N + cnt], opk.extract(ob, cnt, R)), j
+
+
+def test_misaligned_rows():
+    """The stage kernel bulk-copies rows (16-byte granules): the C-ABI rejects misaligned
+    in/out with SFHR_EINVAL, and the Python engine copies a misaligned view first, so its
+    result equals the aligned call's."""
+    import ctypes
+    import torch
+    from paper_2509_01253_b200 import _native as nat
+    sch, ksk, eng = _engine(12, 1)
+    N = sch.ring.N
+    d = sorted(k for k in ksk.keys if k != 1)[0]
+    x = torch.from_numpy(u53(5, (3, 2, N)).view(np.int64)).cuda()
+    big = torch.zeros(3 * 2 * N + 1, dtype=torch.int64, device="cuda")
+    big[1:] = x.reshape(-1)
+    mis = big[1:].view(3, 2, N)
+    assert mis.data_ptr() % 16 == 8
+    ref = eng.switch_batch(x, d)
+    assert torch.equal(eng.switch_batch(mis, d), ref)
+    out = torch.empty_like(x)
+    code = nat.lib.sfhr_keyswitch_batch(eng.ctx.h, eng.key.h, d % eng.ctx.M, nat.ptr(mis), nat.ptr(out), 3, 0,
+                                        None, eng.ctx.stream())
+    assert code == nat.SFHR_EINVAL and "aligned" in nat.last_error()
