@@ -47,6 +47,21 @@ constexpr int EPT = NTT_EPT;     // residues per thread in a local pass
 #ifndef NTT_MINB
 #define NTT_MINB 2
 #endif
+// every global / remote load of a thread's cross-chunk work and of its final chunk pass issued
+// before the first use (the loops were latency-serialised: one round trip per iteration)
+// (bit 0: forward cross-chunk loads, for clusters of <= 2^NTT_FWD_PRE_MAXCL CTAs; bit 1: forward
+// final pass; bit 2: inverse final pass (C = 1); bit 3: inverse cross-chunk DSMEM loads, for
+// clusters of >= 2^NTT_INV_PRE_MINCL CTAs -- below those sizes the 16 prefetched values per
+// thread cost more in registers than the latency they hide)
+#ifndef NTT_BATCH_IO
+#define NTT_BATCH_IO 1
+#endif
+#ifndef NTT_FWD_PRE_MAXCL
+#define NTT_FWD_PRE_MAXCL 2
+#endif
+#ifndef NTT_INV_PRE_MINCL
+#define NTT_INV_PRE_MINCL 3
+#endif
 
 struct Tables {
   const double* w;     // [L][N] psi^brv(k) (forward), k >= 1 used, exact integers
@@ -279,10 +294,24 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd
     // wait just before the first remote store
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     bool waited = false;
-    for (int o = c * (CH / C) + threadIdx.x; o < (c + 1) * (CH / C); o += NT) {
+    constexpr int IT = (CH / C) / NT;  // o-iterations per thread (EPT / C)
+    constexpr bool kPre = (NTT_BATCH_IO & 1) && LOGCL <= NTT_FWD_PRE_MAXCL && IT * C <= EPT;
+    uint64_t pre[kPre ? IT * C : 1];
+    if constexpr (kPre) {
+#pragma unroll
+      for (int it = 0; it < IT; ++it)
+#pragma unroll
+        for (int q = 0; q < C; ++q) pre[it * C + q] = x[(int64_t)q * CH + c * (CH / C) + threadIdx.x + it * NT];
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int o = c * (CH / C) + threadIdx.x + it * NT;
       double v[C];
 #pragma unroll
-      for (int q = 0; q < C; ++q) v[q] = (double)x[(int64_t)q * CH + o];
+      for (int q = 0; q < C; ++q) {
+        if constexpr (kPre) v[q] = (double)pre[it * C + q];
+        else v[q] = (double)x[(int64_t)q * CH + o];
+      }
 #pragma unroll
       for (int s = 0; s < LOGCL; ++s) {
         const int half = C >> (s + 1);
@@ -310,7 +339,15 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd
   }
   fwd_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, wp, p, pinv);
   uint64_t* xo = x + (int64_t)c * CH;
-  for (int i = threadIdx.x; i < CH; i += NT) xo[i] = to_residue(sm[pad(i)], p, pinv);
+  if (NTT_BATCH_IO & 2) {
+    double o[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) o[e] = sm[pad(threadIdx.x + e * NT)];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) xo[threadIdx.x + e * NT] = to_residue(o[e], p, pinv);
+  } else {
+    for (int i = threadIdx.x; i < CH; i += NT) xo[i] = to_residue(sm[pad(i)], p, pinv);
+  }
 }
 
 template <int LOGN, int LOGCL>
@@ -340,15 +377,39 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_inv
   __syncthreads();
   inv_local<LOGC>(sm, (int64_t)c * CH, LOGCL, w, wp, p, pinv);
   if (C == 1) {
-    for (int i = threadIdx.x; i < CH; i += NT)
-      x[i] = to_residue(mulmod_d(red_d(sm[pad(i)], p, pinv), ninv, ninvp, p), p, pinv);
+    if (NTT_BATCH_IO & 4) {
+      double o[EPT];
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) o[e] = sm[pad(threadIdx.x + e * NT)];
+#pragma unroll
+      for (int e = 0; e < EPT; ++e)
+        x[threadIdx.x + e * NT] = to_residue(mulmod_d(red_d(o[e], p, pinv), ninv, ninvp, p), p, pinv);
+    } else {
+      for (int i = threadIdx.x; i < CH; i += NT)
+        x[i] = to_residue(mulmod_d(red_d(sm[pad(i)], p, pinv), ninv, ninvp, p), p, pinv);
+    }
   } else {
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
-    for (int o = c * (CH / C) + threadIdx.x; o < (c + 1) * (CH / C); o += NT) {
+    constexpr int IT = (CH / C) / NT;  // o-iterations per thread (EPT / C)
+    constexpr bool kPre = (NTT_BATCH_IO & 8) && LOGCL >= NTT_INV_PRE_MINCL && IT * C <= EPT;
+    double pre[kPre ? IT * C : 1];
+    if constexpr (kPre) {
+#pragma unroll
+      for (int it = 0; it < IT; ++it)
+#pragma unroll
+        for (int q = 0; q < C; ++q)
+          pre[it * C + q] = cluster.map_shared_rank(sm, q)[pad(c * (CH / C) + threadIdx.x + it * NT)];
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int o = c * (CH / C) + threadIdx.x + it * NT;
       double v[C];
 #pragma unroll
-      for (int q = 0; q < C; ++q) v[q] = red_d(cluster.map_shared_rank(sm, q)[pad(o)], p, pinv);
+      for (int q = 0; q < C; ++q) {
+        if constexpr (kPre) v[q] = red_d(pre[it * C + q], p, pinv);
+        else v[q] = red_d(cluster.map_shared_rank(sm, q)[pad(o)], p, pinv);
+      }
 #pragma unroll
       for (int s = LOGCL - 1; s >= 0; --s) {
         const int half = C >> (s + 1);
