@@ -56,6 +56,12 @@ constexpr int EPT = NTT_EPT;     // residues per thread in a local pass
 #ifndef NTT_BATCH_IO
 #define NTT_BATCH_IO 1
 #endif
+// A/B knob: the next local pass's twiddles prefetched into L1 while the current pass runs (their
+// L2 latency stalls the first butterfly of a pass); measured 1-7 % slower (the prefetch
+// instructions and address math cost more issue slots than the latency they hide), so off
+#ifndef NTT_TW_PREFETCH
+#define NTT_TW_PREFETCH 0
+#endif
 #ifndef NTT_FWD_PRE_MAXCL
 #define NTT_FWD_PRE_MAXCL 2
 #endif
@@ -135,6 +141,55 @@ __device__ __forceinline__ void load_twiddles(int K, double* tw, const double* s
 // Range discipline: every pass reduces on load and after its second stage, so no
 // value exceeds 0.5 p + 2 * 1.5 p < 4 p < 2^52.
 
+__device__ __forceinline__ void prefetch_l1(const void* a) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+}
+// L1 prefetch of the twiddle groups forward pass `pass` of fwd_local will load (same addresses)
+template <int LOGC>
+__device__ __forceinline__ void fwd_tw_prefetch(int pass, int64_t c0, int s0, const double* w) {
+  int done = 0;
+#pragma unroll
+  for (int q = 0; q < (LOGC + 3) / 4; ++q) {
+    if (q == pass) break;
+    done += (q == 0 && (LOGC % 4)) ? (LOGC % 4) : 4;
+  }
+  const int r = (pass == 0 && (LOGC % 4)) ? (LOGC % 4) : 4;
+  const int logD = LOGC - done - 1, D = 1 << logD, inner = D >> (r - 1), per = EPT >> r;
+#pragma unroll
+  for (int h = 0; h < per; ++h) {
+    const int id = threadIdx.x * per + h;
+    const int b = id / inner;
+    const int64_t B0 = c0 + (int64_t)b * 2 * D;
+#pragma unroll
+    for (int st = 0; st < r; ++st)
+      prefetch_l1(w + ((int64_t)1 << (s0 + done + st)) + (B0 >> (logD + 1 - st)));
+  }
+}
+// the same for inverse pass `pass` of inv_local
+template <int LOGC>
+__device__ __forceinline__ void inv_tw_prefetch(int pass, int64_t c0, int s0, const double* w) {
+  constexpr int NP = (LOGC + 3) / 4;
+  int done = 0;
+#pragma unroll
+  for (int q = 0; q < NP; ++q) {
+    if (q == pass) break;
+    done += (q == NP - 1 && (LOGC % 4)) ? (LOGC % 4) : 4;
+  }
+  const int r = (pass == NP - 1 && (LOGC % 4)) ? (LOGC % 4) : 4;
+  const int logD = done + r - 1, D = 1 << logD, inner = 1 << done, per = EPT >> r;
+#pragma unroll
+  for (int h = 0; h < per; ++h) {
+    const int id = threadIdx.x * per + h;
+    const int b = id / inner;
+    const int64_t B0 = c0 + (int64_t)b * 2 * D;
+#pragma unroll
+    for (int u = 0; u < r; ++u) {
+      const int sg = s0 + LOGC - 1 - (done + r - 1 - u);
+      prefetch_l1(w + ((int64_t)1 << sg) + (B0 >> (logD + 1 - u)));
+    }
+  }
+}
+
 // local forward passes over a chunk (global position of element 0 = c0), stages with
 // distance chunk/2 .. 1; s0 = global stage index of the first local stage
 template <int LOGC>
@@ -172,6 +227,7 @@ __device__ __forceinline__ void fwd_local(double* sm, int64_t c0, int s0, const 
         v[h * (1 << r) + lo] = r <= 2 ? red_d(x, p, pinv) : x;
       }
     }
+    if (NTT_TW_PREFETCH && pass + 1 < (LOGC + 3) / 4) fwd_tw_prefetch<LOGC>(pass + 1, c0, s0, w);
 #pragma unroll
     for (int st = 0; st < r; ++st) {
       const int half = (1 << r) >> (st + 1);    // distance in lo units
@@ -238,6 +294,7 @@ __device__ __forceinline__ void inv_local(double* sm, int64_t c0, int s0, const 
         v[h * (1 << r) + lo] = r <= 2 ? red_d(x, p, pinv) : x;
       }
     }
+    if (NTT_TW_PREFETCH && pass + 1 < (LOGC + 3) / 4) inv_tw_prefetch<LOGC>(pass + 1, c0, s0, w);
 #pragma unroll
     for (int st = 0; st < r; ++st) {
       const int half = 1 << st;
@@ -280,6 +337,7 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_fwd
   const double* w = t.w + (size_t)limb * ((size_t)1 << LOGN);
   const double* wp = t.wp + (size_t)limb * ((size_t)1 << LOGN);
   uint64_t* x = data + poly * ((int64_t)1 << LOGN);
+  if (NTT_TW_PREFETCH) fwd_tw_prefetch<LOGC>(0, (int64_t)c * CH, LOGCL, w);
   if (C == 1) {
     uint64_t in[EPT];  // all loads in flight before the first shared store
 #pragma unroll
@@ -363,6 +421,7 @@ __global__ void __launch_bounds__((1 << (LOGN - LOGCL)) / EPT, NTT_MINB) ntt_inv
   const double* wp = t.wip + (size_t)limb * ((size_t)1 << LOGN);
   const double ninv = __ldg(w), ninvp = __ldg(wp);  // wi[0] = N^-1
   uint64_t* x = data + poly * ((int64_t)1 << LOGN);
+  if (NTT_TW_PREFETCH) inv_tw_prefetch<LOGC>(0, (int64_t)c * CH, LOGCL, w);
   const uint64_t* xi = x + (int64_t)c * CH;
   {
     uint64_t in[EPT];  // all loads in flight before the first shared store
