@@ -406,15 +406,15 @@ constexpr bool kItemMajor = T <= 5;
 
 // forward DIF stages s = 0 .. alpha-3 (all but the last, span > 1).  SH: twiddles from the Shoup
 // pairs sh[e / t] (every mid-stage exponent is a multiple of t) instead of the Montgomery table
-template <int T, int A, int PR, bool SH = false>
+template <int T, int A, int PR, bool SH = false, int SKIP = 0>
 __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const RingConst& rc,
                                                const uint32_t* wt, const uint2* sh = nullptr) {
   const PrimeConst& pc = rc.pc[PR];
   const Geo<T, A> g(rc);
   const int nsub = g.n1 / T;
 #pragma unroll
-  for (int s = 0; s < (A ? A - 2 : 16); ++s) {
-    if (!A && s >= g.alpha - 2) break;
+  for (int s = 0; s < (A ? A - 2 - SKIP : 16); ++s) {
+    if (!A && s >= g.alpha - 2 - SKIP) break;
     const int L = A ? cpow(T, A - 2 - s) : nsub / cpow(T, s);
     const int step = g.M / (T * L);
     const int stepT = step / T;  // exact: L <= n1 / T
@@ -469,6 +469,32 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
     }
     __syncthreads();
   }
+}
+
+// The last mid stage (span L = T) fused with the last stage + key MAC (SFHR_FUSE_LAST_MID): a
+// group of T lanes of one warp owns a T x T block of every digit transform -- its T mid-stage
+// items (offset j, stride T), then, after a __syncwarp, its T MAC items (rows of the block) --
+// so no CTA barrier separates the two phases.  Shoup twiddles loaded ahead (SH + TW_EARLY form).
+// Measured slower on B200 (ResNet-20 stage 109.95 vs 105.79 ms: the mid-stage items run on 11
+// of 12 warps with 28 of 32 lanes instead of all 384 threads, and spills grow), so off.
+#ifndef SFHR_FUSE_LAST_MID
+#define SFHR_FUSE_LAST_MID 0
+#endif
+template <int T, int A, int PR>
+__device__ __forceinline__ void fwd_last_mid_item(uint32_t* v, const int j, const RingConst& rc, const uint2* sh) {
+  const PrimeConst& pc = rc.pc[PR];
+  const Geo<T, A> g(rc);
+  const int es = g.M / (T * T * T) * j;  // (step / t) j with step = M / t^2
+  uint2 tw[T];
+#pragma unroll
+  for (int k = 1; k < T; ++k) tw[k] = sh[es * k];
+  uint32_t x[T], y[T];
+#pragma unroll
+  for (int m = 0; m < T; ++m) x[m] = v[m * T];
+  dft_fwd_tw<T>(x, y, pc);
+  v[0] = y[0];
+#pragma unroll
+  for (int k = 1; k < T; ++k) v[k * T] = shoup_mul(y[k], tw[k], pc.p);
 }
 
 // inverse DIT stages s = alpha-3 .. 0 (the span-1 stage is undone in registers)
@@ -780,12 +806,31 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       }
       sync.prefetched = true;
     }
-    fwd_mid_stages<T, A, PR, SFHR_SHOUP_MID>(S.buf, L, rc, S.wt, S.sh);
+    constexpr bool kFuse = SFHR_FUSE_LAST_MID && T == 7 && A >= 3 && SFHR_SHOUP_MID && SFHR_TW_EARLY &&
+                           !kItemMajor<T>;
+    fwd_mid_stages<T, A, PR, SFHR_SHOUP_MID, kFuse ? 1 : 0>(S.buf, L, rc, S.wt, S.sh);
+#ifdef SFHR_T7_THREADS
+    static_assert(!kFuse || A != 4 || SFHR_T7_THREADS >= 352, "the fused MAC needs 42 groups of 7 lanes");
+#endif
+    int mac_item = item;
+    bool mac_owner = owner;
+    if constexpr (kFuse) {
+      constexpr int GPW = 32 / T;  // groups per warp
+      const int lane = threadIdx.x & 31, grp = (threadIdx.x >> 5) * GPW + lane / T, j = lane % T;
+      mac_owner = lane < GPW * T && grp < g.nitems / T;
+      mac_item = grp * T + j;
+      if (mac_owner) {
+#pragma unroll 1
+        for (int i = 0; i < L; ++i) fwd_last_mid_item<T, A, PR>(S.buf + i * N + grp * T * T + j, j, rc, S.sh);
+      }
+      __syncwarp();
+    }
     // the staged mask is dead after the last rep's gathers: tell the peers they may push
     // their CRT residues into it (the matching wait precedes our own pushes)
     if (r == a.nreps - 1 && !a.independent) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     // ---- C: last stage (span 1) in registers, MAC against the key spectra ----
-    if (owner) {
+    if (mac_owner) {
+      const int item = mac_item;
       const uint32_t* ks = a.spec[r];
       uint64_t ta[T], tb[T];
 #pragma unroll
