@@ -639,6 +639,13 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   __shared__ int last_s;
   const uint32_t row_bar = sync.bar_mask;
   if (SFHR_STAGE_BULK) {
+    // the CTA's first row initialises the barriers; the copies are issued before the CTA barrier
+    // that publishes the init, so they overlap it
+    if (threadIdx.x == 0 && stage_twiddles) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sync.bar_mask) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sync.bar_body) : "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
     if (threadIdx.x == 0 && !sync.prefetched) {
       const uint32_t xb = (uint32_t)N * 8u;
       const uint32_t wb = stage_twiddles ? (uint32_t)twid_stride(M) * 4u : 0u;
@@ -650,6 +657,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
         row_bulk(smem_addr(S.sh), a.twid + (size_t)rc.np * twid_stride(M) + (size_t)PR * shoup_stride(n1), hb,
                  row_bar);
     }
+    if (stage_twiddles) __syncthreads();  // the barriers' init is visible
     row_bar_wait(row_bar, sync.ph_mask);
     sync.ph_mask ^= 1u;
     sync.prefetched = false;
@@ -1067,15 +1075,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 template <int T, int A, int L, int PR>
 __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned char* smem, const int64_t item) {
   __shared__ __align__(8) uint64_t bars[2];
-  RowSync sync{smem_addr(&bars[0]), smem_addr(&bars[1]), 0u, 0u, false};
-  if (SFHR_STAGE_BULK) {
-    if (threadIdx.x == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sync.bar_mask) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sync.bar_body) : "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    }
-    __syncthreads();  // the barriers' init is visible
-  }
+  RowSync sync{smem_addr(&bars[0]), smem_addr(&bars[1]), 0u, 0u, false};  // init: first stage_row
   if (a.acc_out && a.nsplit > 1) {  // representative split: item = (row, split)
     const unsigned r = (unsigned)item / (unsigned)a.nsplit;
     stage_row<T, A, L, PR>(rc, a, smem, r, true, sync, -1, (int)((unsigned)item - r * (unsigned)a.nsplit));
