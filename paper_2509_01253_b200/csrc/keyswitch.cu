@@ -608,6 +608,29 @@ __device__ __forceinline__ SmemLayout carve(unsigned char* smem, const RingConst
   return s;
 }
 
+// CRT primes of the compile-time (production) geometries: the planner gives 3 for every preset
+// row; launch_stage takes the A != 0 specialisation only when rc.np matches, so the stage
+// kernel's per-CTA divisions by np and the shared-memory carve-up fold to constants
+constexpr int kProdNP = 3;
+template <int T, int A>
+__device__ __forceinline__ int stage_np(const RingConst& rc) { return A ? kProdNP : rc.np; }
+
+template <int T, int A>
+__device__ __forceinline__ SmemLayout carve_t(unsigned char* smem, const RingConst& rc) {
+  const Geo<T, A> g(rc);
+  const unsigned np = (unsigned)stage_np<T, A>(rc);
+  const unsigned per = ((unsigned)g.N + np - 1u) / np;
+  const unsigned recv = np * 2u * per * 4u, mask = (unsigned)g.N * 8u;
+  const unsigned xa = ((recv > mask ? recv : mask) + 15u) & ~15u;
+  SmemLayout s;
+  s.xa = reinterpret_cast<uint64_t*>(smem);
+  s.wt = reinterpret_cast<uint32_t*>(smem + xa);
+  s.sh = reinterpret_cast<uint2*>(s.wt + twid_stride(g.M));
+  s.acc = s.wt + twid_stride(g.M) + shoup_stride(g.n1);
+  s.buf = s.acc + 2 * g.N;
+  return s;
+}
+
 // bulk-copy completion state of a CTA across its rows: bar_mask completes the row prologue (or
 // the previous row's prefetch of this row's mask), bar_body the body copy of the L2 CRT path
 struct RowSync {
@@ -628,7 +651,9 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   const uint32_t p = pc.p, pinv = pc.pinv, mu = pc.mu;
   const Geo<T, A> g(rc);
   const int N = g.N, n1 = g.n1, M = g.M;
-  SmemLayout S = carve(smem, rc);
+  SmemLayout S = carve_t<T, A>(smem, rc);
+  const int np = stage_np<T, A>(rc);
+  const size_t crw = ((size_t)np * 2 * N + 31) & ~(size_t)31;  // crt_row_words
   const uint64_t* xin = a.in + row * 2 * (int64_t)N;
   uint64_t* xout = a.out + row * 2 * (int64_t)N;
   cg::cluster_group cluster = cg::this_cluster();
@@ -654,7 +679,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       row_bulk(smem_addr(S.xa), xin, xb, row_bar);
       if (wb) row_bulk(smem_addr(S.wt), a.twid + (size_t)PR * twid_stride(M), wb, row_bar);
       if (hb)
-        row_bulk(smem_addr(S.sh), a.twid + (size_t)rc.np * twid_stride(M) + (size_t)PR * shoup_stride(n1), hb,
+        row_bulk(smem_addr(S.sh), a.twid + (size_t)np * twid_stride(M) + (size_t)PR * shoup_stride(n1), hb,
                  row_bar);
     }
     if (stage_twiddles) __syncthreads();  // the barriers' init is visible
@@ -680,7 +705,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     uint4* wdst = reinterpret_cast<uint4*>(S.wt);
     for (int k = threadIdx.x; k < twid_stride(M) / 4; k += blockDim.x) wdst[k] = wsrc[k];
     if (SFHR_SHOUP_MID) {
-      const uint4* hsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)rc.np * twid_stride(M) +
+      const uint4* hsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)np * twid_stride(M) +
                                                          (size_t)PR * shoup_stride(n1));
       uint4* hdst = reinterpret_cast<uint4*>(S.sh);
       for (int k = threadIdx.x; k < shoup_stride(n1) / 4; k += blockDim.x) hdst[k] = hsrc[k];
@@ -691,7 +716,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     for (int k = threadIdx.x; k < N; k += blockDim.x) nz |= xin[N + k] != 0;
     live = __syncthreads_or(nz);
   }
-  const int per = (N + rc.np - 1) / rc.np;
+  const int per = (N + np - 1) / np;
   const int k0 = PR * per, k1 = min(N, k0 + per);
   // this cluster's representatives (all of them unless the launch splits them, acc_out); the
   // split launch counts its own reps, so the acc_in launch that sums the partials does not
@@ -722,7 +747,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {  // 2N u32 = N/2 uint4
       uint4 v = make_uint4(0, 0, 0, 0);
       for (int q = 0; q < parts; ++q) {
-        const uint4 w = reinterpret_cast<const uint4*>(a.acc_in + (((size_t)row * parts + q) * rc.np + PR) * 2 * N)[c];
+        const uint4 w = reinterpret_cast<const uint4*>(a.acc_in + (((size_t)row * parts + q) * np + PR) * 2 * N)[c];
         v.x += w.x;
         v.y += w.y;
         v.z += w.z;
@@ -851,8 +876,8 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
         for (int m = 0; m < T; ++m) x[m] = v[m];
         if constexpr (kLazyMac<L>) dft_fwd_tw<T>(x, yv, pc);  // y_k < 2^32
         else dft_fwd_red<T>(x, yv, pc);
-        const uint32_t* ka = ks + ((size_t)(i * 2 + 0) * rc.np + PR) * N + item;
-        const uint32_t* kb = ks + ((size_t)(i * 2 + 1) * rc.np + PR) * N + item;
+        const uint32_t* ka = ks + ((size_t)(i * 2 + 0) * np + PR) * N + item;
+        const uint32_t* kb = ks + ((size_t)(i * 2 + 1) * np + PR) * N + item;
 #pragma unroll
         for (int k = 0; k < T; ++k) {
           ta[k] += (uint64_t)yv[k] * __ldg(ka + k * g.nitems);
@@ -880,7 +905,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
 
   if (a.acc_out) {  // representative split: hand this cluster's partial sums to the acc_in launch
     uint4* dst = reinterpret_cast<uint4*>(
-        a.acc_out + (((size_t)row * (a.nsplit > 1 ? a.nsplit : 1) + split) * rc.np + PR) * 2 * N);
+        a.acc_out + (((size_t)row * (a.nsplit > 1 ? a.nsplit : 1) + split) * np + PR) * 2 * N);
     const uint4* src = reinterpret_cast<const uint4*>(S.acc);
     for (int c = threadIdx.x; c < N / 2; c += blockDim.x) dst[c] = src[c];
     return;
@@ -958,7 +983,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     double fa = 0.0, fb = 0.0;
 #pragma unroll
     for (int i = 0; i < MAXNP; ++i) {
-      if (i < rc.np) {
+      if (i < np) {
         ua += (uint64_t)ya[i] * rc.pc[i].q_mod64;
         ub += (uint64_t)yb[i] * rc.pc[i].q_mod64;
         fa += (double)ya[i] * rc.pc[i].inv_p;
@@ -975,7 +1000,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     // ---- CRT through L2 (independent CTAs, no cluster): every CTA stores its residues of the
     // whole row, and the last of the row's np CTAs to arrive (device-scope counter) combines
     // them, adds the body term and writes the row; the others exit at once ----
-    uint32_t* rs = a.crt_scratch + (size_t)row * crt_row_words(rc);
+    uint32_t* rs = a.crt_scratch + (size_t)row * crw;
     {
       uint4* mine = reinterpret_cast<uint4*>(rs + (size_t)PR * 2 * N);
       const uint4* src = reinterpret_cast<const uint4*>(S.buf);
@@ -987,7 +1012,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       // acq_rel: releases this CTA's residues and, for the last arriver, acquires the peers'
       unsigned old;
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.crt_cnt + row) : "memory");
-      last_s = old == (unsigned)(rc.np - 1);
+      last_s = old == (unsigned)(np - 1);
     }
     __syncthreads();
     if (body_staged) {  // every CTA: the copy targets its smem
@@ -1013,7 +1038,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       uint32_t ya[MAXNP], yb[MAXNP];
 #pragma unroll
       for (int i = 0; i < MAXNP; ++i) {
-        if (i < rc.np) {
+        if (i < np) {
           ya[i] = i == PR ? S.buf[k] : __ldcg(rs + (size_t)i * 2 * N + k);
           yb[i] = i == PR ? S.buf[N + k] : __ldcg(rs + (size_t)i * 2 * N + N + k);
         }
@@ -1022,7 +1047,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
     __syncthreads();
     // the row's residues are dead: drop their L2 lines without writing them back
-    for (int w = threadIdx.x * 32; w < crt_row_words(rc); w += blockDim.x * 32)
+    for (int w = threadIdx.x * 32; w < crw; w += blockDim.x * 32)
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(rs + w) : "memory");
     return;
   }
@@ -1039,7 +1064,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // peers' masks are dead
   {
     uint32_t* recv = reinterpret_cast<uint32_t*>(S.xa);
-    for (int q = 0; q < rc.np; ++q) {
+    for (int q = 0; q < np; ++q) {
       uint32_t* dst = cluster.map_shared_rank(recv, q) + (size_t)PR * 2 * per;
       const int q0 = q * per, q1 = min(N, q0 + per);
       for (int k = q0 + threadIdx.x; k < q1; k += blockDim.x) {
@@ -1055,7 +1080,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     uint32_t ya[MAXNP], yb[MAXNP];
 #pragma unroll
     for (int i = 0; i < MAXNP; ++i) {
-      if (i < rc.np) {
+      if (i < np) {
         ya[i] = recv[(size_t)i * 2 * per + (k - k0)];
         yb[i] = recv[(size_t)i * 2 * per + per + (k - k0)];
       }
@@ -1112,8 +1137,9 @@ template <int T, int A, int L>
 __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMinBlocks)
     ks_stage_kernel(const __grid_constant__ RingConst rc, const __grid_constant__ StageArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const int np = stage_np<T, A>(rc);
   // item = row (or (row, split) of a representative-split launch) and the CTA's CRT prime
-  int64_t item = blockIdx.x / rc.np;
+  int64_t item = blockIdx.x / np;
   unsigned rank;
   if (!a.independent) {
     rank = cg::this_cluster().block_rank();
@@ -1124,14 +1150,14 @@ __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMin
     const unsigned nitems = (unsigned)(a.acc_out && a.nsplit > 1
                                            ? a.B * a.nsplit
                                            : (a.B + SFHR_ROWS_PER_CLUSTER - 1) / SFHR_ROWS_PER_CLUSTER);
-    const unsigned per_group = (unsigned)a.group * (unsigned)rc.np;
+    const unsigned per_group = (unsigned)a.group * (unsigned)np;
     const unsigned g = blockIdx.x / per_group, base = g * (unsigned)a.group;
     const unsigned gc = nitems - base < (unsigned)a.group ? nitems - base : (unsigned)a.group;
     const unsigned within = blockIdx.x - g * per_group;
     rank = within / gc;
     item = base + (within - rank * gc);
   } else {
-    rank = blockIdx.x % rc.np;
+    rank = blockIdx.x % np;
   }
   switch (rank) {
     case 0: stage_body<T, A, L, 0>(rc, a, smem, item); break;
@@ -1255,7 +1281,7 @@ cudaError_t SFHR_CAT(launch_stage_t, SFHR_KS_T, _l, SFHR_KS_L)(const RingConst& 
                                                               cudaStream_t st) {
   constexpr int T = SFHR_KS_T, L = SFHR_KS_L;
   constexpr int A = T == 7 ? 4 : T == 5 ? 5 : 7;
-  if (rc.alpha == A) return launch_stage_tal<T, A, L>(rc, a, st);
+  if (rc.alpha == A && rc.np == kProdNP) return launch_stage_tal<T, A, L>(rc, a, st);
   return launch_stage_tal<T, 0, L>(rc, a, st);
 }
 #else

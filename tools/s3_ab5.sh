@@ -1,5 +1,5 @@
 #!/bin/bash
-# session-3 A/B 5: prologue copies issued before the barrier-init CTA barrier (main) vs previous HEAD (prev)
+# session-3 A/B 5 / 7: main (working tree) vs prev (HEAD) on ResNet-20 and ResNet-18 + stage GPU tests
 set -u
 bash tools/ab.sh main prev main prev
 BENCH_ARGS="--workload resnet18" bash tools/ab.sh main prev
