@@ -615,6 +615,49 @@ constexpr int kProdNP = 3;
 template <int T, int A>
 __device__ __forceinline__ int stage_np(const RingConst& rc) { return A ? kProdNP : rc.np; }
 
+// gadget base of the preset rows by (t, alpha, l): b=8 (512, 3); b=12
+// (4096, 3) at gamma = 0 and (2^16, 2) above; b=16 (310, 5) / (310, 4).  0: runtime gadget.
+// launch_stage takes the A != 0 specialisation only when rc.D matches
+template <int T, int A, int L>
+__host__ __device__ constexpr int prod_gadget_D() {
+  return !A ? 0
+         : T == 7 && A == 4 ? (L == 3 ? 4096 : L == 2 ? 65536 : 0)
+         : T == 5 && A == 5 ? (L == 5 || L == 4 ? 310 : 0)
+         : T == 3 && A == 7 ? (L == 3 ? 512 : 0)
+         : 0;
+}
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v / 2); }
+
+// balanced digits with the gadget as compile-time constants when the geometry fixes it
+template <int T, int A, int L>
+__device__ __forceinline__ void decompose_t(uint64_t y, int (&dg)[L], const RingConst& rc) {
+  constexpr int DC = prod_gadget_D<T, A, L>();
+  if constexpr (DC == 0) {
+    decompose<L>(y, dg, rc);
+  } else if constexpr ((DC & (DC - 1)) == 0) {
+    constexpr int w = ilog2c(DC), shift = 53 - w * L;
+    uint64_t u = (y + (1ull << (shift - 1))) >> shift;
+    int carry = 0;
+#pragma unroll
+    for (int i = L - 1; i >= 0; --i) {
+      const int x = (int)(u & (uint64_t)(DC - 1)) + carry;
+      u >>= w;
+      carry = x > (DC >> 1);
+      dg[i] = carry ? x - DC : x;
+    }
+  } else {
+    long long r = (long long)y;
+    if (y > (1ull << 52)) r -= (1ll << 53);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const long long prod = r * DC;
+      const long long d = (prod + (1ll << 52)) >> 53;
+      dg[i] = (int)d;
+      r = prod - d * (1ll << 53);
+    }
+  }
+}
+
 template <int T, int A>
 __device__ __forceinline__ SmemLayout carve_t(unsigned char* smem, const RingConst& rc) {
   const Geo<T, A> g(rc);
@@ -780,7 +823,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
         for (int j = 0; j < T - 1; ++j) {
           const uint64_t v1 = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
           int d[L];
-          decompose<L>((v1 - v2) & QMASK, d, rc);
+          decompose_t<T, A, L>((v1 - v2) & QMASK, d, rc);
 #pragma unroll
           for (int i = 0; i < L; ++i) dg[i][j] = d[i];
           s1 += step1;
@@ -822,7 +865,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       uint64_t y = s1 < (uint32_t)N ? S.xa[s1] : 0ull;
       if (s2 < (uint32_t)N) y -= S.xa[s2];
       int dg[L];
-      decompose<L>(y & QMASK, dg, rc);
+      decompose_t<T, A, L>(y & QMASK, dg, rc);
 #pragma unroll
       for (int i = 0; i < L; ++i) S.buf[i * N + k] = lift_signed(dg[i], p);
     }
@@ -1281,7 +1324,8 @@ cudaError_t SFHR_CAT(launch_stage_t, SFHR_KS_T, _l, SFHR_KS_L)(const RingConst& 
                                                               cudaStream_t st) {
   constexpr int T = SFHR_KS_T, L = SFHR_KS_L;
   constexpr int A = T == 7 ? 4 : T == 5 ? 5 : 7;
-  if (rc.alpha == A && rc.np == kProdNP) return launch_stage_tal<T, A, L>(rc, a, st);
+  if (rc.alpha == A && rc.np == kProdNP && rc.D == prod_gadget_D<T, A, L>())
+    return launch_stage_tal<T, A, L>(rc, a, st);
   return launch_stage_tal<T, 0, L>(rc, a, st);
 }
 #else
