@@ -72,6 +72,35 @@ struct Geo {
         nitems(A ? cpow(T, A - 1) * (T - 1) / T : rc.nitems) {}
 };
 
+#ifndef SFHR_T7_THREADS
+#define SFHR_T7_THREADS 384
+#endif
+#ifndef SFHR_T5_THREADS
+#define SFHR_T5_THREADS 512
+#endif
+#ifndef SFHR_T5_MINBLOCKS
+#define SFHR_T5_MINBLOCKS 2
+#endif
+#ifndef SFHR_T7_MINBLOCKS
+#define SFHR_T7_MINBLOCKS 3
+#endif
+template <int T>
+struct StageLaunch {
+  static constexpr int kThreads = T == 7 ? SFHR_T7_THREADS : T == 5 ? SFHR_T5_THREADS : 512;
+  static constexpr int kMinBlocks = T == 7 ? SFHR_T7_MINBLOCKS : T == 5 ? SFHR_T5_MINBLOCKS : 2;
+};
+
+// block size: the launch-bound constant for the compile-time geometries (stage_threads launches
+// them with exactly kThreads), so block-strided loops have compile-time trip counts.  Not for
+// t = 7: at its 56-register cap the unrolled loops spill ~1 KB (SFHR_BDIM_T7 A/B knob)
+#ifndef SFHR_BDIM_T7
+#define SFHR_BDIM_T7 0
+#endif
+template <int T, int A>
+__device__ __forceinline__ int bdim() {
+  return A && (T != 7 || SFHR_BDIM_T7) ? StageLaunch<T>::kThreads : (int)blockDim.x;
+}
+
 // ---------------------------------------------------------------------------
 // small DFT helper (constants come from the __grid_constant__ parameter block
 // at compile-time offsets -> uniform-register operands of IMAD.WIDE.U32)
@@ -369,7 +398,7 @@ __device__ __forceinline__ void fwd_first_step(uint32_t* buf, int nb, const Ring
                                                const uint32_t* wt) {
   const PrimeConst& pc = rc.pc[PR];
   const Geo<T, A> g(rc);
-  for (int w = threadIdx.x; w < g.n1 * nb; w += blockDim.x) {
+  for (int w = threadIdx.x; w < g.n1 * nb; w += bdim<T, A>()) {
     const int i = w / g.n1, m = w - i * g.n1;
     uint32_t* v = buf + i * g.N + m;
     uint32_t vals[T - 1];
@@ -450,7 +479,7 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
     if constexpr (kItemMajor<T>) {
       // item-major, buffers inner: position and twiddle exponent computed once for all nb
       // transforms (A/B on B200: t = 5 stage kernel -6 %; t = 7 +3 %, so t = 7 stays flat)
-      for (int it = threadIdx.x; it < g.nitems; it += blockDim.x) {
+      for (int it = threadIdx.x; it < g.nitems; it += bdim<T, A>()) {
         const int sub = it / nsub, rem = it - sub * nsub;
         const int b = rem / L, j = rem - b * L;
         const int off = sub * g.n1 + b * T * L + j;
@@ -461,7 +490,7 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
       // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
       // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
       // (two constant divisions instead of three; none at the first stage, where L = nsub)
-      for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
+      for (int w = threadIdx.x; w < g.nitems * nb; w += bdim<T, A>()) {
         const int P = w / nsub, r = w - P * nsub;
         const int b = L == nsub ? 0 : r / L, j = r - b * L;
         item(buf + P * g.n1 + r + b * (T - 1) * L, j);
@@ -528,7 +557,7 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
       for (int m = 0; m < T; ++m) v[m * L] = x[m];
     };
     if constexpr (kItemMajor<T>) {
-      for (int it = threadIdx.x; it < g.nitems; it += blockDim.x) {
+      for (int it = threadIdx.x; it < g.nitems; it += bdim<T, A>()) {
         const int sub = it / nsub, rem = it - sub * nsub;
         const int b = rem / L, j = rem - b * L;
         const int off = sub * g.n1 + b * T * L + j;
@@ -539,7 +568,7 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
       // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
       // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
       // (two constant divisions instead of three; none at the first stage, where L = nsub)
-      for (int w = threadIdx.x; w < g.nitems * nb; w += blockDim.x) {
+      for (int w = threadIdx.x; w < g.nitems * nb; w += bdim<T, A>()) {
         const int P = w / nsub, r = w - P * nsub;
         const int b = L == nsub ? 0 : r / L, j = r - b * L;
         item(buf + P * g.n1 + r + b * (T - 1) * L, j);
@@ -555,7 +584,7 @@ __device__ __forceinline__ void inv_first_step(uint32_t* buf, int nb, const Ring
                                                const uint32_t* wt) {
   const PrimeConst& pc = rc.pc[PR];
   const Geo<T, A> g(rc);
-  for (int w = threadIdx.x; w < g.n1 * nb; w += blockDim.x) {
+  for (int w = threadIdx.x; w < g.n1 * nb; w += bdim<T, A>()) {
     const int q = w / g.n1, m = w - q * g.n1;
     uint32_t* v = buf + q * g.N + m;
     uint32_t C[T - 1];
@@ -730,14 +759,14 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     sync.ph_mask ^= 1u;
     sync.prefetched = false;
     const uint4* src = reinterpret_cast<const uint4*>(S.xa);
-    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {
+    for (int c = threadIdx.x; c < N / 2; c += bdim<T, A>()) {
       const uint4 v = src[c];
       nz |= (v.x | v.y | v.z | v.w) != 0;
     }
   } else {
     const uint4* src = reinterpret_cast<const uint4*>(xin);  // rows are 16-byte aligned (N even)
     uint4* dst = reinterpret_cast<uint4*>(S.xa);
-    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {
+    for (int c = threadIdx.x; c < N / 2; c += bdim<T, A>()) {
       const uint4 v = src[c];
       dst[c] = v;
       nz |= (v.x | v.y | v.z | v.w) != 0;
@@ -746,17 +775,17 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   if (stage_twiddles && !SFHR_STAGE_BULK) {
     const uint4* wsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)PR * twid_stride(M));
     uint4* wdst = reinterpret_cast<uint4*>(S.wt);
-    for (int k = threadIdx.x; k < twid_stride(M) / 4; k += blockDim.x) wdst[k] = wsrc[k];
+    for (int k = threadIdx.x; k < twid_stride(M) / 4; k += bdim<T, A>()) wdst[k] = wsrc[k];
     if (SFHR_SHOUP_MID) {
       const uint4* hsrc = reinterpret_cast<const uint4*>(a.twid + (size_t)np * twid_stride(M) +
                                                          (size_t)PR * shoup_stride(n1));
       uint4* hdst = reinterpret_cast<uint4*>(S.sh);
-      for (int k = threadIdx.x; k < shoup_stride(n1) / 4; k += blockDim.x) hdst[k] = hsrc[k];
+      for (int k = threadIdx.x; k < shoup_stride(n1) / 4; k += bdim<T, A>()) hdst[k] = hsrc[k];
     }
   }
   int live = __syncthreads_or(nz);
   if (!live) {
-    for (int k = threadIdx.x; k < N; k += blockDim.x) nz |= xin[N + k] != 0;
+    for (int k = threadIdx.x; k < N; k += bdim<T, A>()) nz |= xin[N + k] != 0;
     live = __syncthreads_or(nz);
   }
   const int per = (N + np - 1) / np;
@@ -768,7 +797,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   const bool counts = !(a.acc_in && a.nsplit > 1);
   if (!live) {
     if (!a.acc_out)
-      for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      for (int k = k0 + threadIdx.x; k < k1; k += bdim<T, A>()) {
         xout[k] = 0;
         xout[N + k] = 0;
       }
@@ -787,7 +816,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     // total stays below 2 p nreps, as in one pass)
     const int parts = a.nsplit > 1 ? a.nsplit : 1;
     uint4* dst = reinterpret_cast<uint4*>(S.acc);
-    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) {  // 2N u32 = N/2 uint4
+    for (int c = threadIdx.x; c < N / 2; c += bdim<T, A>()) {  // 2N u32 = N/2 uint4
       uint4 v = make_uint4(0, 0, 0, 0);
       for (int q = 0; q < parts; ++q) {
         const uint4 w = reinterpret_cast<const uint4*>(a.acc_in + (((size_t)row * parts + q) * np + PR) * 2 * N)[c];
@@ -809,7 +838,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     // transform step for every digit straight from registers ----
     {
       const uint32_t step1 = fastmod((uint32_t)n1 * dinv, M, rc.magicM);
-      for (int m = threadIdx.x; m < n1; m += blockDim.x) {
+      for (int m = threadIdx.x; m < n1; m += bdim<T, A>()) {
         const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
         const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
         uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
@@ -858,7 +887,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
 #else
     // ---- A: automorphism gather + digits of every coefficient ----
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    for (int k = threadIdx.x; k < N; k += bdim<T, A>()) {
       const uint32_t km = (uint32_t)(k % n1);
       const uint32_t s1 = fastmod((uint32_t)k * dinv, M, rc.magicM);
       const uint32_t s2 = fastmod((uint32_t)(N + km) * dinv, M, rc.magicM);
@@ -950,7 +979,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     uint4* dst = reinterpret_cast<uint4*>(
         a.acc_out + (((size_t)row * (a.nsplit > 1 ? a.nsplit : 1) + split) * np + PR) * 2 * N);
     const uint4* src = reinterpret_cast<const uint4*>(S.acc);
-    for (int c = threadIdx.x; c < N / 2; c += blockDim.x) dst[c] = src[c];
+    for (int c = threadIdx.x; c < N / 2; c += bdim<T, A>()) dst[c] = src[c];
     return;
   }
 
@@ -1047,7 +1076,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     {
       uint4* mine = reinterpret_cast<uint4*>(rs + (size_t)PR * 2 * N);
       const uint4* src = reinterpret_cast<const uint4*>(S.buf);
-      for (int c = threadIdx.x; c < N / 2; c += blockDim.x) mine[c] = src[c];  // 2N u32
+      for (int c = threadIdx.x; c < N / 2; c += bdim<T, A>()) mine[c] = src[c];  // 2N u32
     }
     // release: the barrier orders the CTA's stores before thread 0's gpu-scope fence (cumulative)
     __syncthreads();
@@ -1077,7 +1106,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       }
       return bsum;
     };
-    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    for (int k = threadIdx.x; k < N; k += bdim<T, A>()) {
       uint32_t ya[MAXNP], yb[MAXNP];
 #pragma unroll
       for (int i = 0; i < MAXNP; ++i) {
@@ -1090,7 +1119,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     }
     __syncthreads();
     // the row's residues are dead: drop their L2 lines without writing them back
-    for (int w = threadIdx.x * 32; w < crw; w += blockDim.x * 32)
+    for (int w = threadIdx.x * 32; w < crw; w += bdim<T, A>() * 32)
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(rs + w) : "memory");
     return;
   }
@@ -1098,7 +1127,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   // ---- body term of this CTA's slice, into the (now free) accumulator region while the
   // other CTAs of the cluster finish ----
   uint64_t* bsum_s = reinterpret_cast<uint64_t*>(S.acc);  // (k1 - k0) u64 <= N u64
-  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) bsum_s[k - k0] = body_sum(k);
+  for (int k = k0 + threadIdx.x; k < k1; k += bdim<T, A>()) bsum_s[k - k0] = body_sum(k);
 
   // ---- explicit CRT across the cluster through distributed shared memory (push) ----
   // every CTA stores its residues of each peer's slice into that peer's (dead) mask
@@ -1110,7 +1139,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     for (int q = 0; q < np; ++q) {
       uint32_t* dst = cluster.map_shared_rank(recv, q) + (size_t)PR * 2 * per;
       const int q0 = q * per, q1 = min(N, q0 + per);
-      for (int k = q0 + threadIdx.x; k < q1; k += blockDim.x) {
+      for (int k = q0 + threadIdx.x; k < q1; k += bdim<T, A>()) {
         dst[k - q0] = S.buf[k];
         dst[per + k - q0] = S.buf[N + k];
       }
@@ -1119,7 +1148,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   const uint32_t* recv = reinterpret_cast<const uint32_t*>(S.xa);
-  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+  for (int k = k0 + threadIdx.x; k < k1; k += bdim<T, A>()) {
     uint32_t ya[MAXNP], yb[MAXNP];
 #pragma unroll
     for (int i = 0; i < MAXNP; ++i) {
@@ -1158,23 +1187,6 @@ __device__ void stage_body(const RingConst& rc, const StageArgs& a, unsigned cha
   }
 }
 
-#ifndef SFHR_T7_THREADS
-#define SFHR_T7_THREADS 384
-#endif
-#ifndef SFHR_T5_THREADS
-#define SFHR_T5_THREADS 512
-#endif
-#ifndef SFHR_T5_MINBLOCKS
-#define SFHR_T5_MINBLOCKS 2
-#endif
-#ifndef SFHR_T7_MINBLOCKS
-#define SFHR_T7_MINBLOCKS 3
-#endif
-template <int T>
-struct StageLaunch {
-  static constexpr int kThreads = T == 7 ? SFHR_T7_THREADS : T == 5 ? SFHR_T5_THREADS : 512;
-  static constexpr int kMinBlocks = T == 7 ? SFHR_T7_MINBLOCKS : T == 5 ? SFHR_T5_MINBLOCKS : 2;
-};
 
 template <int T, int A, int L>
 __global__ void __launch_bounds__(StageLaunch<T>::kThreads, StageLaunch<T>::kMinBlocks)
@@ -1294,6 +1306,8 @@ static cudaError_t launch_stage_tal(const RingConst& rc, const StageArgs& a, cud
                                                      : (a.B + SFHR_ROWS_PER_CLUSTER - 1) / SFHR_ROWS_PER_CLUSTER;
   cfg.gridDim = dim3((unsigned)(clusters * rc.np), 1, 1);
   cfg.blockDim = dim3(stage_threads(rc), 1, 1);
+  // the compile-time geometries stride their loops by the launch-bound block size (bdim)
+  if (A && cfg.blockDim.x != (unsigned)StageLaunch<T>::kThreads) return cudaErrorInvalidConfiguration;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
