@@ -91,10 +91,17 @@ struct StageLaunch {
 };
 
 // block size: the launch-bound constant for the compile-time geometries (stage_threads launches
-// them with exactly kThreads), so block-strided loops have compile-time trip counts.  Not for
-// t = 7: at its 56-register cap the unrolled loops spill ~1 KB (SFHR_BDIM_T7 A/B knob)
+// them with exactly kThreads), so block-strided loops have compile-time trip counts.  At t = 7
+// (56-register cap) the compiler would unroll them into ~1 KB of spills, so there they stay
+// rolled (SFHR_T7_LOOP); SFHR_BDIM_T7=0 keeps blockDim.x for t = 7
 #ifndef SFHR_BDIM_T7
-#define SFHR_BDIM_T7 0
+#define SFHR_BDIM_T7 1
+#endif
+// with the constant stride at t = 7 the block-strided loops are kept rolled (the unrolled ones spill)
+#if SFHR_BDIM_T7
+#define SFHR_T7_LOOP _Pragma("unroll 1")
+#else
+#define SFHR_T7_LOOP
 #endif
 template <int T, int A>
 __device__ __forceinline__ int bdim() {
@@ -490,6 +497,7 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
       // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
       // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
       // (two constant divisions instead of three; none at the first stage, where L = nsub)
+      SFHR_T7_LOOP
       for (int w = threadIdx.x; w < g.nitems * nb; w += bdim<T, A>()) {
         const int P = w / nsub, r = w - P * nsub;
         const int b = L == nsub ? 0 : r / L, j = r - b * L;
@@ -568,6 +576,7 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
       // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
       // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
       // (two constant divisions instead of three; none at the first stage, where L = nsub)
+      SFHR_T7_LOOP
       for (int w = threadIdx.x; w < g.nitems * nb; w += bdim<T, A>()) {
         const int P = w / nsub, r = w - P * nsub;
         const int b = L == nsub ? 0 : r / L, j = r - b * L;
@@ -584,7 +593,7 @@ __device__ __forceinline__ void inv_first_step(uint32_t* buf, int nb, const Ring
                                                const uint32_t* wt) {
   const PrimeConst& pc = rc.pc[PR];
   const Geo<T, A> g(rc);
-  for (int w = threadIdx.x; w < g.n1 * nb; w += bdim<T, A>()) {
+  auto untwist = [&](const int w) {
     const int q = w / g.n1, m = w - q * g.n1;
     uint32_t* v = buf + q * g.N + m;
     uint32_t C[T - 1];
@@ -604,6 +613,12 @@ __device__ __forceinline__ void inv_first_step(uint32_t* buf, int nb, const Ring
         v[j * g.n1] = fully(redc(s, pc.p, pc.pinv), pc.p);
       }
     }
+  };
+  if constexpr (T == 7) {
+    SFHR_T7_LOOP
+    for (int w = threadIdx.x; w < g.n1 * nb; w += bdim<T, A>()) untwist(w);
+  } else {
+    for (int w = threadIdx.x; w < g.n1 * nb; w += bdim<T, A>()) untwist(w);
   }
   __syncthreads();
 }
@@ -838,7 +853,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     // transform step for every digit straight from registers ----
     {
       const uint32_t step1 = fastmod((uint32_t)n1 * dinv, M, rc.magicM);
-      for (int m = threadIdx.x; m < n1; m += bdim<T, A>()) {
+      auto column = [&](const int m) {
         const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
         const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
         uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
@@ -882,6 +897,12 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
           }
 #endif
         }
+      };
+      if constexpr (T == 7) {
+        SFHR_T7_LOOP
+        for (int m = threadIdx.x; m < n1; m += bdim<T, A>()) column(m);
+      } else {
+        for (int m = threadIdx.x; m < n1; m += bdim<T, A>()) column(m);
       }
       __syncthreads();
     }
