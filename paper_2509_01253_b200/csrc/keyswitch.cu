@@ -103,6 +103,15 @@ struct StageLaunch {
 #else
 #define SFHR_T7_LOOP
 #endif
+// x mod M: a constant division for the compile-time geometries (SFHR_CT_MOD; -0.1 %)
+#ifndef SFHR_CT_MOD
+#define SFHR_CT_MOD 1
+#endif
+template <int T, int A>
+__device__ __forceinline__ uint32_t mod_m(uint32_t x, const RingConst& rc) {
+  if constexpr (A != 0 && SFHR_CT_MOD) return x % (uint32_t)cpow(T, A);
+  else return fastmod(x, (uint32_t)rc.M, rc.magicM);
+}
 template <int T, int A>
 __device__ __forceinline__ int bdim() {
   return A && (T != 7 || SFHR_BDIM_T7) ? StageLaunch<T>::kThreads : (int)blockDim.x;
@@ -421,6 +430,15 @@ __device__ __forceinline__ void fwd_first_step(uint32_t* buf, int nb, const Ring
   }
   __syncthreads();
 }
+
+// digits of the key MAC loop: unrolled at t = 7 (the next digit's key-spectrum loads issue during
+// this digit's DFT: ResNet-20 stage -2.6 %, no spills), rolled at t = 3 / 5 (+2.9 % at t = 5).
+// SFHR_MAC_UNROLL = 0: rolled everywhere
+#ifndef SFHR_MAC_UNROLL
+#define SFHR_MAC_UNROLL 1
+#endif
+template <int T, int L>
+constexpr int kMacUnroll = SFHR_MAC_UNROLL && T == 7 ? L : 1;
 
 // lazy MAC pays off from three digits on (one Barrett per accumulator vs one per digit)
 template <int L>
@@ -852,11 +870,11 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
     // aut(x.a), decompose them (carry chain, all digits), and run the first
     // transform step for every digit straight from registers ----
     {
-      const uint32_t step1 = fastmod((uint32_t)n1 * dinv, M, rc.magicM);
+      const uint32_t step1 = mod_m<T, A>((uint32_t)n1 * dinv, rc);
       auto column = [&](const int m) {
-        const uint32_t s2 = fastmod((uint32_t)(N + m) * dinv, M, rc.magicM);
+        const uint32_t s2 = mod_m<T, A>((uint32_t)(N + m) * dinv, rc);
         const uint64_t v2 = s2 < (uint32_t)N ? S.xa[s2] : 0ull;
-        uint32_t s1 = fastmod((uint32_t)m * dinv, M, rc.magicM);
+        uint32_t s1 = mod_m<T, A>((uint32_t)m * dinv, rc);
         int dg[L][T - 1];
         uint32_t tw[T];  // first-step twists omega^(q m), shared by the l digit transforms
         if (SFHR_TW_EARLY) {
@@ -961,7 +979,7 @@ __device__ __forceinline__ void stage_row(const RingConst& rc, const StageArgs& 
       uint64_t ta[T], tb[T];
 #pragma unroll
       for (int k = 0; k < T; ++k) ta[k] = tb[k] = 0;
-#pragma unroll 1
+#pragma unroll(kMacUnroll<T, L>)
       for (int i = 0; i < L; ++i) {
         const uint32_t* v = S.buf + i * N + item * T;
         uint32_t x[T], yv[T];
