@@ -103,6 +103,12 @@ struct StageLaunch {
 #else
 #define SFHR_T7_LOOP
 #endif
+// the flat mid-stage loops (t = 7) -- A/B knob SFHR_T7_MID_UNROLL2: unrolled by 2
+#if SFHR_BDIM_T7 && SFHR_T7_MID_UNROLL2
+#define SFHR_T7_MID_LOOP _Pragma("unroll 2")
+#else
+#define SFHR_T7_MID_LOOP SFHR_T7_LOOP
+#endif
 // x mod M: a constant division for the compile-time geometries (SFHR_CT_MOD; -0.1 %)
 #ifndef SFHR_CT_MOD
 #define SFHR_CT_MOD 1
@@ -515,7 +521,7 @@ __device__ __forceinline__ void fwd_mid_stages(uint32_t* buf, int nb, const Ring
       // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
       // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
       // (two constant divisions instead of three; none at the first stage, where L = nsub)
-      SFHR_T7_LOOP
+      SFHR_T7_MID_LOOP
       for (int w = threadIdx.x; w < g.nitems * nb; w += bdim<T, A>()) {
         const int P = w / nsub, r = w - P * nsub;
         const int b = L == nsub ? 0 : r / L, j = r - b * L;
@@ -594,7 +600,7 @@ __device__ __forceinline__ void inv_mid_stages(uint32_t* buf, int nb, const Ring
       // w = q nitems + sub nsub + b L + j; with N = (T-1) n1 the buffer offset
       // q N + sub n1 + b T L + j is P n1 + r + b (T-1) L for P = w / nsub, r = w mod nsub
       // (two constant divisions instead of three; none at the first stage, where L = nsub)
-      SFHR_T7_LOOP
+      SFHR_T7_MID_LOOP
       for (int w = threadIdx.x; w < g.nitems * nb; w += bdim<T, A>()) {
         const int P = w / nsub, r = w - P * nsub;
         const int b = L == nsub ? 0 : r / L, j = r - b * L;
