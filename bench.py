@@ -335,7 +335,7 @@ def stage_traffic(N):
     algorithmic 32 N bytes per row (rows = grid / 3 CTAs per cluster); the capture
     is of the b = 12 (N = 2058) ResNet-20 stem pack, so the ratio is only quoted
     for that ring."""
-    f = ROOT / "profiles" / "r02i" / "ncu_stage_summary.json"
+    f = ROOT / "profiles" / "r02j" / "ncu_stage_summary.json"
     try:
         launches = [l for l in json.loads(f.read_text())["launches"] if "ks_stage_kernel" in l["kernel"]]
     except Exception:
